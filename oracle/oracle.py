@@ -1,0 +1,189 @@
+"""ctypes front-end for the CPU oracle (TEST INFRASTRUCTURE ONLY).
+
+Only tests/, __graft_entry__.smoke() and bench.py's cpu_baseline /
+``--impl reference`` arm may import this module -- as the checker, never as
+the thing measured or shipped.  The product package never imports it.
+
+The heavy lifting is in intattn_oracle.c (a plain-C restatement of the
+reference path, see its header).  ``build_lut`` is restated here in numpy
+because the reference builds its table with numpy's f64 ``exp``
+(softmax.py:88-102); using the same exp keeps the table bytes identical.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+import subprocess
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_SO = os.path.join(_HERE, "liboracle.so")
+_lib = None
+
+P_UINT8X255 = 255
+P_INT8X127 = 127
+
+
+def build() -> str:
+    """Compile liboracle.so in place (gcc; see Makefile)."""
+    src = os.path.join(_HERE, "intattn_oracle.c")
+    if not os.path.exists(_SO) or os.path.getmtime(_SO) < os.path.getmtime(src):
+        subprocess.run(["make", "-s", "-C", _HERE], check=True)
+    return _SO
+
+
+def lib():
+    global _lib
+    if _lib is None:
+        if not os.path.exists(_SO):
+            build()
+        L = ctypes.CDLL(_SO)
+        P = ctypes.c_void_p
+        i64 = ctypes.c_int64
+        L.ia_or_amax.restype = ctypes.c_float
+        L.ia_or_amax.argtypes = [P, i64, P]
+        L.ia_or_scale.restype = ctypes.c_float
+        L.ia_or_scale.argtypes = [ctypes.c_float]
+        L.ia_or_quantize.argtypes = [P, i64, ctypes.c_float, P]
+        L.ia_or_c_int.restype = i64
+        L.ia_or_c_int.argtypes = [ctypes.c_double, i64, ctypes.c_float, ctypes.c_float]
+        L.ia_or_matmul_s8.argtypes = [P, P, i64, i64, i64, P]
+        L.ia_or_gemm_pv.argtypes = [P, P, i64, i64, i64, P]
+        L.ia_or_index_softmax.argtypes = [P, i64, i64, i64, P, ctypes.c_int,
+                                          ctypes.c_int, P, P]
+        L.ia_or_attention_batched.restype = ctypes.c_int
+        L.ia_or_attention_batched.argtypes = [
+            P, P, P, i64, i64, i64, i64, i64, P, ctypes.c_int, P, ctypes.c_int,
+            ctypes.c_double, P, ctypes.c_int, ctypes.c_int, i64, ctypes.c_int,
+            P, P, P, P, P]
+        _lib = L
+    return _lib
+
+
+def _p(a):
+    return None if a is None else a.ctypes.data_as(ctypes.c_void_p)
+
+
+# --------------------------------------------------------------------------
+# Host-side constants (numpy, as the reference computes them)
+# --------------------------------------------------------------------------
+
+def build_lut(b: int = 5, c: float = 6.6) -> np.ndarray:
+    """lut[i] = round_half_away(255*exp(-c*i/(2^b-1))) in f64, lut[last] = 0
+    (softmax.py:88-102; rounding.py:12-21)."""
+    n = 1 << b
+    x = 255.0 * np.exp(-c * np.arange(n, dtype=np.float64) / (n - 1))
+    e = np.copysign(np.floor(np.abs(x) + 0.5), x).astype(np.uint8)
+    e[n - 1] = 0
+    return e
+
+
+def index_table(c_int: int, n_entries: int) -> np.ndarray:
+    """itab[delta] = (2*delta*k + c)//(2c) (softmax.py:124-128)."""
+    k = n_entries - 1
+    delta = np.arange(c_int, dtype=np.int64)
+    return ((2 * delta * k + c_int) // (2 * c_int)).astype(np.uint8)
+
+
+# --------------------------------------------------------------------------
+# Stage functions (small sizes; used by per-stage parity tests)
+# --------------------------------------------------------------------------
+
+def quantize_tensor(x: np.ndarray):
+    """Per-tensor quantise_symmetric: returns (int8 values, f32 scale)."""
+    x = np.ascontiguousarray(x, dtype=np.float32)
+    bad = ctypes.c_int(0)
+    amax = lib().ia_or_amax(_p(x), x.size, ctypes.byref(bad))
+    if bad.value:
+        raise ValueError("input contains non-finite elements")
+    s = np.float32(lib().ia_or_scale(amax))
+    out = np.empty(x.shape, np.int8)
+    lib().ia_or_quantize(_p(x), x.size, s, _p(out))
+    return out, s
+
+
+def quantize_groups(x: np.ndarray, n_groups: int):
+    """Row-major contiguous groups (per-row-group / per-head): (values, scales)."""
+    x = np.ascontiguousarray(x, dtype=np.float32)
+    flat = x.reshape(n_groups, -1)
+    out = np.empty(flat.shape, np.int8)
+    scales = np.empty(n_groups, np.float32)
+    for g in range(n_groups):
+        bad = ctypes.c_int(0)
+        amax = lib().ia_or_amax(_p(flat[g]), flat.shape[1], ctypes.byref(bad))
+        if bad.value:
+            raise ValueError("input contains non-finite elements")
+        scales[g] = lib().ia_or_scale(amax)
+        lib().ia_or_quantize(_p(flat[g]), flat.shape[1], scales[g], _p(out[g]))
+    return out.reshape(x.shape), scales
+
+
+def c_int(c: float, d: int, s_q: float, s_k: float) -> int:
+    return int(lib().ia_or_c_int(float(c), int(d), float(s_q), float(s_k)))
+
+
+def matmul_s8(a: np.ndarray, b_t: np.ndarray) -> np.ndarray:
+    a = np.ascontiguousarray(a, np.int8)
+    b_t = np.ascontiguousarray(b_t, np.int8)
+    out = np.empty((a.shape[0], b_t.shape[0]), np.int32)
+    lib().ia_or_matmul_s8(_p(a), _p(b_t), a.shape[0], b_t.shape[0], a.shape[1], _p(out))
+    return out
+
+
+def gemm_pv(p: np.ndarray, v: np.ndarray) -> np.ndarray:
+    p = np.ascontiguousarray(p).view(np.uint8)
+    v = np.ascontiguousarray(v, np.int8)
+    out = np.empty((p.shape[0], v.shape[1]), np.int32)
+    lib().ia_or_gemm_pv(_p(p), _p(v), p.shape[0], p.shape[1], v.shape[1], _p(out))
+    return out
+
+
+def index_softmax(logits: np.ndarray, ci: int, lut: np.ndarray, mask=None,
+                  p_scale: int = P_UINT8X255) -> np.ndarray:
+    logits = np.ascontiguousarray(logits, np.int32)
+    lut = np.ascontiguousarray(lut, np.uint8)
+    m8 = None if mask is None else np.ascontiguousarray(mask).astype(np.uint8)
+    out = np.empty(logits.shape, np.uint8)
+    lib().ia_or_index_softmax(_p(logits), logits.shape[0], logits.shape[1], int(ci),
+                              _p(lut), lut.size, int(p_scale), _p(m8), _p(out))
+    return out
+
+
+def int_attention(q, k, v, b=5, c=6.6, mask=None, p_scale=P_UINT8X255):
+    """Single-head reference pipeline (pipeline.py:202-256) -> f32 [L, d]."""
+    q = np.ascontiguousarray(q, np.float32)
+    out, _ = attention_batched(q[None, None], np.asarray(k, np.float32)[None, None],
+                               np.asarray(v, np.float32)[None, None], mask=mask,
+                               b=b, c=c, p_scale=p_scale)
+    return out[0, 0]
+
+
+def attention_batched(q, k, v, *, causal=False, seq_lens=None, mask=None,
+                      scale_granularity="head", b=5, c=6.6, p_scale=P_UINT8X255,
+                      row_stride=1, threads=0, lut=None):
+    """Batched oracle (see ia_or_attention_batched).  Returns (out, info)."""
+    q = np.ascontiguousarray(q, np.float32)
+    k = np.ascontiguousarray(k, np.float32)
+    v = np.ascontiguousarray(v, np.float32)
+    B, H, L, d = q.shape
+    Hkv = k.shape[1]
+    lut = build_lut(b, c) if lut is None else np.ascontiguousarray(lut, np.uint8)
+    sl = None if seq_lens is None else np.ascontiguousarray(seq_lens, np.int32)
+    m8 = None if mask is None else np.ascontiguousarray(mask).astype(np.uint8)
+    out = np.zeros(q.shape, np.float32)
+    qs = np.empty(B * H, np.float32)
+    ks = np.empty(B * Hkv, np.float32)
+    vs = np.empty(B * Hkv, np.float32)
+    ci = np.empty(B * H, np.int64)
+    mode = {"head": 0, "tensor": 1}[scale_granularity]
+    st = lib().ia_or_attention_batched(
+        _p(q), _p(k), _p(v), B, H, Hkv, L, d, _p(sl), int(bool(causal)), _p(m8),
+        mode, float(c), _p(lut), lut.size, int(p_scale), int(row_stride),
+        int(threads), _p(out), _p(qs), _p(ks), _p(vs), _p(ci))
+    if st == 1:
+        raise ValueError("input contains non-finite elements")
+    if st != 0:
+        raise ValueError(f"oracle rejected arguments (status {st})")
+    return out, {"q_scales": qs, "k_scales": ks, "v_scales": vs, "c_int": ci}
