@@ -1,0 +1,157 @@
+/*
+ * intattn_b200.h -- C ABI of the B200 (sm_100a) IntAttention forward path.
+ *
+ * Plain pointers and sizes only (no torch types).  All device pointers are
+ * CUDA device memory; `stream` is a cudaStream_t passed as void*.  Calls are
+ * asynchronous and stream-ordered; buffers are caller-allocated.  Every entry
+ * point returns an ia_status (0 = ok).  The reference is a Python package
+ * (intattn) with no FFI of its own, so each entry point below names the
+ * reference operator it replaces (paths relative to
+ * /root/reference/pkg/src/intattn/); INTEGRATION.md shows the ctypes binding.
+ */
+#ifndef INTATTN_B200_H
+#define INTATTN_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define IA_ABI_VERSION 1
+#define IA_MAX_SEQ_LEN 65536   /* gemm.py:26 MAX_SEQ_LEN */
+#define IA_MAX_HEAD_DIM 131070 /* gemm.py:25 MAX_HEAD_DIM */
+#define IA_FUSED_MAX_HEAD_DIM 256
+
+typedef enum ia_status {
+  IA_OK = 0,
+  IA_ERR_INVALID_ARGUMENT = 1, /* shape/range errors: the reference's ValueError */
+  IA_ERR_SEQ_LEN = 2,          /* L > 65536 (pipeline.py:91-92, gemm.py:130-131) */
+  IA_ERR_HEAD_DIM = 3,         /* d outside this entry point's range */
+  IA_ERR_NONFINITE = 4,        /* non-finite input (quantize.py:109-110) */
+  IA_ERR_CUDA = 5,             /* CUDA runtime/driver failure (see ia_last_error) */
+  IA_ERR_NO_DEVICE = 6,        /* no sm_100 device */
+  IA_ERR_LUT = 7               /* LUT endpoints not 255/0 (softmax.py:230-234) */
+} ia_status;
+
+int ia_abi_version(void);
+const char* ia_status_string(int status);
+/* Human-readable detail of the last failure on the calling thread. */
+const char* ia_last_error(void);
+/* Returns IA_OK if device `dev` is an sm_100 part this library can run on. */
+int ia_device_check(int dev);
+
+/* ------------------------------------------------------------------ quantiser
+ * Replaces quantize_symmetric (quantize.py:104-123) and _group_maxabs
+ * (quantize.py:92-101).  Two stream-ordered steps: amax (atomic max of the
+ * f32 bit pattern into caller-zeroed amax_bits) then quantise.
+ *
+ * Row layout: x is [n_rowgroups * rows_per_group, cols] f32, row-major.
+ * Row group g has valid_rows[g / valid_div] valid rows when valid_rows is
+ * non-NULL (seq_lens for padded batches), else rows_per_group.  Its max |x|
+ * over valid rows is folded into slot g / slot_div (slot_div = 1: one scale
+ * per row group / head; slot_div = n_rowgroups: one global scale).
+ * err_flag (device int32) is set to 1 if any valid element is non-finite.
+ */
+int ia_quant_amax_rows(const float* x, int64_t n_rowgroups, int64_t rows_per_group,
+                       int64_t cols, const int32_t* valid_rows, int64_t valid_div,
+                       int64_t slot_div, uint32_t* amax_bits, int32_t* err_flag,
+                       void* stream);
+/* Per-column-group max |x| (per_col_group granularity, quantize.py:99-101). */
+int ia_quant_amax_cols(const float* x, int64_t rows, int64_t cols, int64_t col_group,
+                       uint32_t* amax_bits, int32_t* err_flag, void* stream);
+/* scales[i] = max(amax[i], 1e-12f) / 127f in IEEE f32 (quantize.py:113). */
+int ia_quant_scales(const uint32_t* amax_bits, int64_t n, float* scales, void* stream);
+
+#define IA_QMODE_ROWS 0 /* scale index (r / rows_per_group) / slot_div */
+#define IA_QMODE_COLS 1 /* scale index c / col_group */
+/* values = clip(round_half_away(x / scale), -127, 127) (quantize.py:121-122).
+ * transpose = 0: out is [rows, out_pitch] int8; columns [cols, out_pitch) and
+ *   invalid rows are written 0 (zero K padding keeps dot products exact).
+ * transpose = 1 (ROWS mode only): out holds, per row group g at
+ *   out + g * out_group_stride, the [cols, out_pitch] transpose (V^T layout
+ *   for the fused kernel's P.V operand); invalid rows are written 0. */
+int ia_quantize(const float* x, int64_t n_rowgroups, int64_t rows_per_group, int64_t cols,
+                const int32_t* valid_rows, int64_t valid_div, int mode, int64_t slot_div,
+                int64_t col_group, const float* scales, int8_t* out, int64_t out_pitch,
+                int transpose, int64_t out_group_stride, void* stream);
+/* out = f32(values) * scale (quantize.py:126-128), same scale indexing. */
+int ia_dequantize(const int8_t* values, int64_t rows, int64_t cols, int mode,
+                  int64_t group, const float* scales, float* out, void* stream);
+
+/* ------------------------------------------------------------------ per-head parameters
+ * c_int = max(1, min(round_half_away(c / alpha), 2^52)), alpha =
+ * f64(s_q) f64(s_k) / sqrt(d) (gemm.py:105, softmax.py:105-121), plus the
+ * exact magic-number form of idx = (2 k delta' + c) // (2c) used on device and
+ * the output scale f32(f64(s_v) / p_scale) (pipeline.py:250-252). */
+typedef struct ia_head_params {
+  int64_t c_int;    /* the reference's c_int */
+  int64_t c_eff;    /* min(c_int, 2k*2*d*127^2 + 1): same idx for every logit */
+  uint32_t magic;   /* idx = umulhi(n, magic) >> shift, n = 2k*delta' + c_eff */
+  int32_t shift;
+  int32_t use32;    /* 1: the 32-bit magic path is exact for every reachable n */
+  float out_scale;
+  float s_q, s_k, s_v;
+  int32_t reserved;
+} ia_head_params;
+
+int ia_head_params_host(double c, int64_t d, int nlut, int p_scale, float s_q, float s_k,
+                        float s_v, ia_head_params* out);
+/* Index-map parameters for a given c_int (clamped to 2^52 as softmax.py:277)
+ * and an upper bound on delta = rowmax - logit (2^32 - 1 covers any int32
+ * logits); used with ia_index_softmax. */
+int ia_softmax_params_host(int64_t c_int, int64_t delta_bound, int nlut, ia_head_params* out);
+/* One entry per (b, h) query unit; *_per_head = 0 selects scales[0]. */
+int ia_head_params_dev(const float* q_scales, const float* k_scales, const float* v_scales,
+                       int q_per_head, int kv_per_head, int64_t B, int64_t H, int64_t Hkv,
+                       int64_t d, double c, int nlut, int p_scale, ia_head_params* out,
+                       void* stream);
+
+/* Pack a bool [L, L] mask (nonzero = excluded) into bits [L, ceil(L/32)]. */
+int ia_mask_pack(const uint8_t* mask, int64_t L, uint32_t* bits, void* stream);
+
+/* ------------------------------------------------------------------ fused attention
+ * Replaces the per-head body of int_attention (pipeline.py:215-253):
+ * gemm_qk -> index_softmax -> gemm_pv -> rescale, fused per (b, h, 128-row
+ * query tile); the int32 logits and u8 probabilities stay in TMEM/registers.
+ * Requires d <= 256 and d_pad in {32, 64, 128, 256} (d_pad >= d); L <= 65536;
+ * H % Hkv == 0 (query head h reads KV head h / (H / Hkv)). */
+typedef struct ia_attn_args {
+  const int8_t* q;   /* [B*H, L, d_pad] quantised Q (pad columns zero) */
+  const int8_t* k;   /* [B*Hkv, L, d_pad] quantised K (pad columns zero) */
+  const int8_t* vt;  /* [B*Hkv, d_pad, l_pad] quantised V, transposed per head */
+  float* out;        /* [B*H, L, d] f32 */
+  const ia_head_params* params; /* [B*H] device */
+  const int32_t* seq_lens;      /* [B] device or NULL: query/key rows >= len are padding */
+  const uint32_t* mask_bits;    /* [L, ceil(L/32)] device or NULL (1 = excluded) */
+  int64_t B, H, Hkv, L, d, d_pad, l_pad;
+  int32_t causal;    /* key j > query i excluded */
+  int32_t nlut;      /* 2^b, 4..256 */
+  int32_t p_scale;   /* 255 (UINT8X255) or 127 (INT8X127) */
+  uint8_t lut[256];  /* ExpLut entries (softmax.py:88-102) */
+  int32_t* dbg_logits; /* optional [B*H, L, L] int32 (debug/parity dump) */
+  uint8_t* dbg_prob;   /* optional [B*H, L, L] u8 */
+  int32_t* dbg_acc;    /* optional [B*H, L, d_pad] int32 */
+} ia_attn_args;
+
+int ia_attn_fwd(const ia_attn_args* args, void* stream);
+
+/* ------------------------------------------------------------------ stage operators
+ * index_softmax (softmax.py:265-299 / :131-204): logits [rows, cols] int32,
+ * optional mask [rows, cols] u8 (nonzero = excluded), out [rows, cols] u8.
+ * hp is a HOST pointer (from ia_head_params_host; c_eff/magic/shift/use32). */
+int ia_index_softmax(const int32_t* logits, int64_t rows, int64_t cols,
+                     const ia_head_params* hp, const uint8_t* lut, int nlut, int p_scale,
+                     const uint8_t* mask, uint8_t* out, void* stream);
+
+/* Exact int8 GEMM on tcgen05 (matmul_int8 / gemm_qk / gemm_pv, gemm.py:45-133):
+ * C[M, N] int32 = A[M, K] * B[N, K]^T; A is s8 (a_signed = 1) or u8; B is s8.
+ * lda/ldb are byte pitches (multiples of 16); ldc in elements. */
+int ia_gemm_i8(const void* A, int64_t lda, int a_signed, const int8_t* B, int64_t ldb,
+               int64_t M, int64_t N, int64_t K, int32_t* C, int64_t ldc, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* INTATTN_B200_H */

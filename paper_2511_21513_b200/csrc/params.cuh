@@ -1,0 +1,123 @@
+// params.cuh -- per-(b, head) IndexSoftmax parameters, shared by host and device.
+#pragma once
+#include <cmath>
+#include <climits>
+#include <cstdint>
+
+#include "intattn_b200.h"
+
+namespace ia {
+
+constexpr int64_t kCIntCap = int64_t(1) << 52;  // softmax.py:47 _C_INT_CAP
+
+// c_int = max(1, min(round_half_away(c / alpha), 2^52)),
+// alpha = f64(s_q) * f64(s_k) / sqrt(d)            (gemm.py:105, softmax.py:105-121)
+// Every operation is a single IEEE f64 op (no contraction possible), so host
+// and device agree bit for bit with Python's float arithmetic.
+__host__ __device__ inline int64_t compute_c_int(double c, int64_t d, float s_q, float s_k) {
+  double alpha = (double)s_q * (double)s_k;
+  alpha = alpha / sqrt((double)d);
+  double r = c / alpha;
+  double t = floor(fabs(r) + 0.5);
+  if (!(t < (double)kCIntCap)) return kCIntCap;
+  int64_t ci = (int64_t)t;
+  return ci < 1 ? 1 : ci;
+}
+
+__host__ __device__ inline int bitlen_u64(uint64_t x) {
+  int n = 0;
+  while (x) { ++n; x >>= 1; }
+  return n;
+}
+
+// Fill everything except the scales.  k = nlut - 1.
+//
+// Index map (softmax.py:144-153):  delta = m - a >= 0;  idx = k if delta >= c_int
+// else (2*delta*k + c_int) // (2*c_int).  With delta' = min(delta, c) this is
+// idx = (2*k*delta' + c) // (2c) for all delta (delta' = c gives k + 1/2 -> k).
+//
+// c_eff: |a| <= d*127^2 so delta <= dbound = 2*d*127^2.  If c_int > 2k*dbound
+// every unmasked idx is 0, and c_eff = 2k*dbound + 1 gives the same (2k*delta
+// < c_eff).  Otherwise c_eff = c_int.  Then n = 2k*delta' + c_eff lies in
+// [c_eff, n_max], n_max = min((2k+1) c_eff, 2k*dbound + c_eff).
+//
+// Magic division: D = 2 c_eff, s = max(0, bitlen(n_max*D - 1) - 32),
+// M = ceil(2^(32+s) / D), e = M*D - 2^(32+s) in [0, D).  For n <= n_max,
+// n*M / 2^(32+s) = n/D + n*e/(D 2^(32+s)) and n*e < n_max*D <= 2^(32+s), so the
+// error term is below 1/D and floor(n*M / 2^(32+s)) = floor(n / D).
+// use32 requires n_max < 2^31 (then M < 2^32); else the kernels divide in 64-bit.
+// dbound: an upper bound on delta = m - a over the logits this map will see
+// (2*d*127^2 for int8 operands; 2^32 - 1 for arbitrary int32 logits).
+__host__ __device__ inline void fill_head_params(int64_t c_int, int64_t dbound, int nlut,
+                                                 ia_head_params* hp) {
+  const int64_t k = nlut - 1;
+  const int64_t clamp = 2 * k * dbound + 1;
+  const int64_t c_eff = c_int < clamp ? c_int : clamp;
+  int64_t n_max = 2 * k * dbound + c_eff;
+  const int64_t alt = (2 * k + 1) * c_eff;
+  if (alt < n_max) n_max = alt;
+  hp->c_int = c_int;
+  hp->c_eff = c_eff;
+  hp->use32 = 0;
+  hp->magic = 0;
+  hp->shift = 0;
+  if (n_max < (int64_t(1) << 31)) {
+    const uint64_t D = 2 * (uint64_t)c_eff;
+    const uint64_t prod = (uint64_t)n_max * D;  // < 2^63
+    int s = bitlen_u64(prod - 1) - 32;            // smallest s with prod <= 2^(32+s)
+    if (s < 0) s = 0;
+    const uint64_t num = uint64_t(1) << (32 + s);
+    const uint64_t M = (num + D - 1) / D;
+    if (M < (uint64_t(1) << 32)) {
+      hp->use32 = 1;
+      hp->magic = (uint32_t)M;
+      hp->shift = s;
+    }
+  }
+}
+
+__host__ __device__ inline void make_head_params(double c, int64_t d, int nlut, int p_scale,
+                                                 float s_q, float s_k, float s_v,
+                                                 ia_head_params* hp) {
+  fill_head_params(compute_c_int(c, d, s_q, s_k), 2 * d * 127 * 127, nlut, hp);
+  hp->out_scale = (float)((double)s_v / (double)p_scale);  // pipeline.py:250
+  hp->s_q = s_q;
+  hp->s_k = s_k;
+  hp->s_v = s_v;
+  hp->reserved = 0;
+}
+
+#ifdef __CUDACC__
+// Per-element index map (softmax.py:144-153), exact magic-number form (params.cuh).
+struct IdxMap {
+  int32_t lo;     // max(m - c_eff, INT32_MIN): a' = max(a, lo) clips delta to c_eff
+  uint32_t base;  // 2k*m + c_eff (mod 2^32)
+  uint32_t k2;    // 2k
+  uint32_t magic;
+  int shift;
+  __device__ __forceinline__ uint32_t idx(int32_t a) const {
+    const int32_t ac = max(a, lo);
+    const uint32_t n = base - k2 * (uint32_t)ac;  // n = 2k*delta' + c_eff in [c_eff, n_max]
+    return __umulhi(n, magic) >> shift;
+  }
+  __device__ __forceinline__ uint32_t idx_masked() const {
+    const uint32_t n = base - k2 * (uint32_t)lo;
+    return __umulhi(n, magic) >> shift;
+  }
+};
+
+// lo for a row max m.  If m - c_eff < INT32_MIN no int32 logit is clipped.
+__device__ __forceinline__ int32_t idx_lo(int32_t m, int64_t c_eff) {
+  const int64_t lo = (int64_t)m - c_eff;
+  return lo < (int64_t)INT32_MIN ? INT32_MIN : (int32_t)lo;
+}
+
+__device__ __forceinline__ uint32_t idx_slow(int64_t m, int32_t a, int64_t c_eff, int64_t k) {
+  int64_t dl = m - (int64_t)a;
+  if (dl > c_eff) dl = c_eff;
+  return (uint32_t)((2 * dl * k + c_eff) / (2 * c_eff));
+}
+
+#endif
+
+}  // namespace ia

@@ -1,0 +1,349 @@
+"""Device-side driver of the B200 IntAttention path.
+
+Owns the stream-ordered launch sequence over the C ABI (include/intattn_b200.h):
+
+    amax(Q), amax(K), amax(V) -> scales -> quantise Q, K (row layout, zero-padded
+    head dim) and V (transposed V^T layout) -> per-(b, h) parameters (c_int,
+    exact index magic numbers, output scale) -> fused attention kernel.
+
+PyTorch supplies device memory, the current stream and host<->device copies;
+every byte of arithmetic runs in the library's sm_100a kernels.  There is no
+CPU fallback: without the library or an sm_100 device every entry raises.
+
+Shapes follow the batched contract of SURVEY.md §8b: q [B, H, L, d],
+k/v [B, Hkv, L, d] f32; query head h attends with KV head h // (H // Hkv).
+"""
+from __future__ import annotations
+
+import ctypes
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import _lib
+
+MAX_SEQ_LEN = 65536
+FUSED_MAX_HEAD_DIM = 256
+
+
+def require_device() -> torch.device:
+    if not torch.cuda.is_available():
+        raise RuntimeError("paper_2511_21513_b200 requires an sm_100 CUDA device; "
+                           "there is no CPU fallback")
+    L = _lib.load()
+    dev = torch.cuda.current_device()
+    _lib.check(L.ia_device_check(dev), "device check")
+    return torch.device("cuda", dev)
+
+
+def _p(t):
+    return None if t is None else ctypes.c_void_p(t.data_ptr())
+
+
+def _stream():
+    return ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+
+
+def pad_head_dim(d: int) -> int | None:
+    for p in (32, 64, 128, 256):
+        if d <= p:
+            return p
+    return None
+
+
+def _round_up(x: int, m: int) -> int:
+    return (x + m - 1) // m * m
+
+
+@dataclass
+class QuantOut:
+    values: torch.Tensor   # int8, layout depends on caller
+    scales: torch.Tensor   # f32 [n_slots]
+
+
+class Workspace:
+    """Per-call scratch: amax bit slots (zeroed) + the non-finite flag."""
+
+    def __init__(self, n_slots: int, device):
+        self.buf = torch.zeros(n_slots + 1, dtype=torch.int32, device=device)
+        self.amax = self.buf[:n_slots]
+        self.err = self.buf[n_slots:]
+        self.scales = torch.empty(n_slots, dtype=torch.float32, device=device)
+        self._off = 0
+
+    def take(self, n: int):
+        a = self.amax[self._off:self._off + n]
+        s = self.scales[self._off:self._off + n]
+        self._off += n
+        return a, s
+
+
+def amax_rows(x, n_groups, rows_per_group, cols, amax, err, *, seq_lens=None, valid_div=1,
+              slot_div=1):
+    L = _lib.load()
+    _lib.check(L.ia_quant_amax_rows(_p(x), n_groups, rows_per_group, cols, _p(seq_lens),
+                                    valid_div, slot_div, _p(amax), _p(err), _stream()), "amax")
+
+
+def scales_from_amax(amax, scales):
+    _lib.check(_lib.load().ia_quant_scales(_p(amax), amax.numel(), _p(scales), _stream()),
+               "scales")
+
+
+def quantize_rows(x, n_groups, rows_per_group, cols, scales, out, out_pitch, *, seq_lens=None,
+                  valid_div=1, slot_div=1, mode=_lib.IA_QMODE_ROWS, col_group=1):
+    _lib.check(_lib.load().ia_quantize(_p(x), n_groups, rows_per_group, cols, _p(seq_lens),
+                                       valid_div, mode, slot_div, col_group, _p(scales), _p(out),
+                                       out_pitch, 0, 0, _stream()), "quantize")
+
+
+def quantize_vt(x, n_groups, rows, cols, scales, out, out_pitch, group_stride, *, seq_lens=None,
+                valid_div=1, slot_div=1):
+    _lib.check(_lib.load().ia_quantize(_p(x), n_groups, rows, cols, _p(seq_lens), valid_div,
+                                       _lib.IA_QMODE_ROWS, slot_div, 1, _p(scales), _p(out),
+                                       out_pitch, 1, group_stride, _stream()), "quantize V^T")
+
+
+def pack_mask(mask: torch.Tensor) -> torch.Tensor:
+    """bool/u8 [L, L] (True = excluded) -> u32 bits [L, ceil(L/32)] on device."""
+    L = mask.shape[0]
+    m8 = mask.to(torch.uint8).contiguous()
+    bits = torch.empty((L, (L + 31) // 32), dtype=torch.int32, device=mask.device)
+    _lib.check(_lib.load().ia_mask_pack(_p(m8), L, _p(bits), _stream()), "mask pack")
+    return bits
+
+
+def raise_if_nonfinite(err: torch.Tensor):
+    if int(err.item()) != 0:
+        raise ValueError("input contains non-finite elements")
+
+
+@dataclass
+class Prepared:
+    """Quantised operands + per-head parameters, ready for the fused kernel."""
+    qhat: torch.Tensor    # [B*H, L, d_pad] int8
+    khat: torch.Tensor    # [B*Hkv, L, d_pad] int8
+    vt: torch.Tensor      # [B*Hkv, d_pad, l_pad] int8
+    q_scales: torch.Tensor
+    k_scales: torch.Tensor
+    v_scales: torch.Tensor
+    params: torch.Tensor  # [B*H] ia_head_params (raw bytes)
+    err: torch.Tensor
+    d_pad: int
+    l_pad: int
+
+
+HEAD_PARAMS_BYTES = ctypes.sizeof(_lib.HeadParams)
+
+
+def prepare(q, k, v, *, seq_lens=None, scale_granularity="head", b=5, c=6.6, p_scale=255,
+            d_pad=None) -> Prepared:
+    """Quantise Q/K/V on device and compute per-(b, h) parameters."""
+    B, H, Lq, d = q.shape
+    Hkv = k.shape[1]
+    dev = q.device
+    if d_pad is None:
+        d_pad = pad_head_dim(d)
+    l_pad = _round_up(Lq, 16)
+    per_head = scale_granularity == "head"
+    nq = B * H if per_head else 1
+    nkv = B * Hkv if per_head else 1
+    ws = Workspace(nq + 2 * nkv, dev)
+    aq, sq = ws.take(nq)
+    ak, sk = ws.take(nkv)
+    av, sv = ws.take(nkv)
+    sl = seq_lens
+    amax_rows(q, B * H, Lq, d, aq, ws.err, seq_lens=sl, valid_div=H,
+              slot_div=1 if per_head else B * H)
+    amax_rows(k, B * Hkv, Lq, d, ak, ws.err, seq_lens=sl, valid_div=Hkv,
+              slot_div=1 if per_head else B * Hkv)
+    amax_rows(v, B * Hkv, Lq, d, av, ws.err, seq_lens=sl, valid_div=Hkv,
+              slot_div=1 if per_head else B * Hkv)
+    scales_from_amax(ws.amax, ws.scales)
+    qhat = torch.empty((B * H, Lq, d_pad), dtype=torch.int8, device=dev)
+    khat = torch.empty((B * Hkv, Lq, d_pad), dtype=torch.int8, device=dev)
+    vt = torch.empty((B * Hkv, d_pad, l_pad), dtype=torch.int8, device=dev)
+    quantize_rows(q, B * H, Lq, d, sq, qhat, d_pad, seq_lens=sl, valid_div=H,
+                  slot_div=1 if per_head else B * H)
+    quantize_rows(k, B * Hkv, Lq, d, sk, khat, d_pad, seq_lens=sl, valid_div=Hkv,
+                  slot_div=1 if per_head else B * Hkv)
+    quantize_vt(v, B * Hkv, Lq, d, sv, vt, l_pad, d_pad * l_pad, seq_lens=sl, valid_div=Hkv,
+                slot_div=1 if per_head else B * Hkv)
+    params = torch.empty((B * H, HEAD_PARAMS_BYTES), dtype=torch.uint8, device=dev)
+    _lib.check(_lib.load().ia_head_params_dev(_p(sq), _p(sk), _p(sv), int(per_head),
+                                              int(per_head), B, H, Hkv, d, float(c), 1 << b,
+                                              int(p_scale), _p(params), _stream()), "head params")
+    return Prepared(qhat, khat, vt, sq, sk, sv, params, ws.err, d_pad, l_pad)
+
+
+def attn_fused(prep: Prepared, shape, out, *, causal=False, seq_lens=None, mask_bits=None,
+               lut=None, p_scale=255, debug=None):
+    B, H, Hkv, Lq, d = shape
+    a = _lib.AttnArgs()
+    a.q, a.k, a.vt = prep.qhat.data_ptr(), prep.khat.data_ptr(), prep.vt.data_ptr()
+    a.out = out.data_ptr()
+    a.params = prep.params.data_ptr()
+    a.seq_lens = None if seq_lens is None else seq_lens.data_ptr()
+    a.mask_bits = None if mask_bits is None else mask_bits.data_ptr()
+    a.B, a.H, a.Hkv, a.L, a.d, a.d_pad, a.l_pad = B, H, Hkv, Lq, d, prep.d_pad, prep.l_pad
+    a.causal = int(bool(causal))
+    a.nlut = len(lut)
+    a.p_scale = int(p_scale)
+    for i, x in enumerate(lut):
+        a.lut[i] = int(x)
+    if debug is not None:
+        a.dbg_logits = debug["logits"].data_ptr()
+        a.dbg_prob = debug["prob"].data_ptr()
+        a.dbg_acc = debug["acc"].data_ptr()
+    _lib.check(_lib.load().ia_attn_fwd(ctypes.byref(a), _stream()), "attention")
+
+
+def lut_bytes(b: int, c: float) -> np.ndarray:
+    """ExpLut entries (softmax.py:88-102), computed on the host in f64 as the
+    reference does: a per-call host constant, not device work."""
+    n = 1 << b
+    x = 255.0 * np.exp(-c * np.arange(n, dtype=np.float64) / (n - 1))
+    e = np.copysign(np.floor(np.abs(x) + 0.5), x).astype(np.uint8)
+    e[n - 1] = 0
+    return e
+
+
+def attention(q, k, v, *, causal=False, seq_lens=None, mask=None, scale_granularity="head",
+              b=5, c=6.6, p_scale=255, lut=None, out=None, debug=False, check_finite=True,
+              timer=None):
+    """Batched fused IntAttention on the current CUDA device.
+
+    q [B, H, L, d], k/v [B, Hkv, L, d]: f32 CUDA tensors (contiguous).
+    seq_lens: int32 CUDA [B] or None.  mask: bool CUDA [L, L] (True = excluded)
+    shared by every unit, or None.  Returns out [B, H, L, d] f32 (and, with
+    debug=True, a dict with the quantised operands, int32 logits, u8 P and int32
+    P.V accumulators for parity checks).
+    """
+    B, H, Lq, d = q.shape
+    Hkv = k.shape[1]
+    if lut is None:
+        lut = lut_bytes(b, c)
+    if out is None:
+        out = torch.empty((B, H, Lq, d), dtype=torch.float32, device=q.device)
+    if timer is not None:
+        timer.mark("start")
+    d_pad = pad_head_dim(d)
+    if d_pad is None:
+        res = _attention_unfused(q, k, v, causal=causal, seq_lens=seq_lens, mask=mask,
+                                 scale_granularity=scale_granularity, b=b, c=c,
+                                 p_scale=p_scale, lut=lut, out=out, check_finite=check_finite)
+        if timer is not None:
+            timer.mark("quantized")
+            timer.mark("attention")
+        return (res, {}) if debug else res
+    prep = prepare(q, k, v, seq_lens=seq_lens, scale_granularity=scale_granularity, b=b, c=c,
+                   p_scale=p_scale, d_pad=d_pad)
+    mbits = pack_mask(mask) if mask is not None else None
+    if timer is not None:
+        timer.mark("quantized")
+    dbg = None
+    if debug:
+        dbg = {"logits": torch.zeros((B * H, Lq, Lq), dtype=torch.int32, device=q.device),
+               "prob": torch.zeros((B * H, Lq, Lq), dtype=torch.uint8, device=q.device),
+               "acc": torch.zeros((B * H, Lq, d_pad), dtype=torch.int32, device=q.device)}
+    attn_fused(prep, (B, H, Hkv, Lq, d), out, causal=causal, seq_lens=seq_lens,
+               mask_bits=mbits, lut=lut, p_scale=p_scale, debug=dbg)
+    if timer is not None:
+        timer.mark("attention")
+    if check_finite:
+        raise_if_nonfinite(prep.err)
+    if debug:
+        dbg.update(qhat=prep.qhat, khat=prep.khat, vt=prep.vt, q_scales=prep.q_scales,
+                   k_scales=prep.k_scales, v_scales=prep.v_scales, params=prep.params)
+        return out, dbg
+    return out
+
+
+def gemm_i8(a, b_t, *, a_signed=True):
+    """C = a @ b_t^T (int32) on tcgen05.  a [M, K] int8/uint8, b_t [N, K] int8 (CUDA)."""
+    M, K = a.shape
+    N = b_t.shape[0]
+    kp = _round_up(K, 16)
+    if kp != K or not a.is_contiguous():
+        a = torch.nn.functional.pad(a.contiguous(), (0, kp - K))
+    if kp != K or not b_t.is_contiguous():
+        b_t = torch.nn.functional.pad(b_t.contiguous(), (0, kp - K))
+    out = torch.empty((M, N), dtype=torch.int32, device=a.device)
+    _lib.check(_lib.load().ia_gemm_i8(_p(a), kp, int(a_signed), _p(b_t), kp, M, N, K, _p(out),
+                                      N, _stream()), "gemm_i8")
+    return out
+
+
+def index_softmax_dev(logits, c_int, lut, mask=None, p_scale=255, delta_bound=(1 << 32) - 1):
+    rows, cols = logits.shape
+    lut_t = torch.as_tensor(np.ascontiguousarray(lut, np.uint8)).to(logits.device)
+    hp = _lib.softmax_params_host(c_int, delta_bound, len(lut))
+    m8 = None if mask is None else mask.to(torch.uint8).contiguous()
+    out = torch.empty((rows, cols), dtype=torch.uint8, device=logits.device)
+    _lib.check(_lib.load().ia_index_softmax(_p(logits), rows, cols, ctypes.byref(hp), _p(lut_t),
+                                            len(lut), int(p_scale), _p(m8), _p(out), _stream()),
+               "index_softmax")
+    return out
+
+
+def _attention_unfused(q, k, v, *, causal, seq_lens, mask, scale_granularity, b, c, p_scale,
+                       lut, out, check_finite):
+    """d > 256: per-unit stage kernels (tcgen05 GEMM -> row IndexSoftmax -> tcgen05 GEMM)."""
+    B, H, Lq, d = q.shape
+    Hkv = k.shape[1]
+    g = H // Hkv
+    per_head = scale_granularity == "head"
+    dp = _round_up(d, 16)
+    lp = _round_up(Lq, 16)
+    nq = B * H if per_head else 1
+    nkv = B * Hkv if per_head else 1
+    ws = Workspace(nq + 2 * nkv, q.device)
+    aq, sq = ws.take(nq)
+    ak, sk = ws.take(nkv)
+    av, sv = ws.take(nkv)
+    amax_rows(q, B * H, Lq, d, aq, ws.err, seq_lens=seq_lens, valid_div=H,
+              slot_div=1 if per_head else B * H)
+    amax_rows(k, B * Hkv, Lq, d, ak, ws.err, seq_lens=seq_lens, valid_div=Hkv,
+              slot_div=1 if per_head else B * Hkv)
+    amax_rows(v, B * Hkv, Lq, d, av, ws.err, seq_lens=seq_lens, valid_div=Hkv,
+              slot_div=1 if per_head else B * Hkv)
+    scales_from_amax(ws.amax, ws.scales)
+    qhat = torch.empty((B * H, Lq, dp), dtype=torch.int8, device=q.device)
+    khat = torch.empty((B * Hkv, Lq, dp), dtype=torch.int8, device=q.device)
+    vt = torch.empty((B * Hkv, dp, lp), dtype=torch.int8, device=q.device)
+    quantize_rows(q, B * H, Lq, d, sq, qhat, dp, seq_lens=seq_lens, valid_div=H,
+                  slot_div=1 if per_head else B * H)
+    quantize_rows(k, B * Hkv, Lq, d, sk, khat, dp, seq_lens=seq_lens, valid_div=Hkv,
+                  slot_div=1 if per_head else B * Hkv)
+    quantize_vt(v, B * Hkv, Lq, d, sv, vt, lp, dp * lp, seq_lens=seq_lens, valid_div=Hkv,
+                slot_div=1 if per_head else B * Hkv)
+    if check_finite:
+        raise_if_nonfinite(ws.err)
+    sq_h, sk_h, sv_h = sq.cpu().numpy(), sk.cpu().numpy(), sv.cpu().numpy()
+    lens = None if seq_lens is None else seq_lens.cpu().numpy()
+    for bb in range(B):
+        n = Lq if lens is None else int(lens[bb])
+        for h in range(H):
+            u, ku = bb * H + h, bb * Hkv + h // g
+            qs = sq_h[u if per_head else 0]
+            ks = sk_h[ku if per_head else 0]
+            vs = sv_h[ku if per_head else 0]
+            hp = _lib.head_params_host(c, d, 1 << b, p_scale, qs, ks, vs)
+            o = out[bb, h]
+            o.zero_()
+            if n == 0:
+                continue
+            logits = gemm_i8(qhat[u, :n], khat[ku, :n])
+            m = None
+            if causal:
+                m = torch.ones((n, n), dtype=torch.bool, device=q.device).triu_(1)
+            if mask is not None:
+                mm = mask[:n, :n]
+                m = mm if m is None else (m | mm)
+            prob = index_softmax_dev(logits, hp.c_int, lut, m, p_scale,
+                                     delta_bound=2 * d * 127 * 127)
+            acc = gemm_i8(prob, vt[ku, :, :n], a_signed=False)
+            o[:n] = acc[:, :d].to(torch.float32) * torch.tensor(hp.out_scale, dtype=torch.float32,
+                                                                  device=q.device)
+    return out

@@ -1,0 +1,200 @@
+"""GPU parity: the CUDA path against the reference's golden vectors and the oracle.
+
+Bit-exact is the bar for every integer/byte stage: quantised
+Q/K/V and scales, int32 logits, u8 P^, int32 P.V and the f32 output bits.
+Run on a B200 with ``pytest -m gpu``.
+"""
+import numpy as np
+import pytest
+import torch
+
+import paper_2511_21513_b200 as ia
+from paper_2511_21513_b200 import engine as E
+from cases import case_inputs, digest
+from golden_io import f32, stage_cases
+from oracle import oracle as O
+
+pytestmark = pytest.mark.gpu
+CASES = stage_cases()
+
+
+def _first_diff(a, b):
+    a, b = np.asarray(a), np.asarray(b)
+    bad = np.argwhere(a != b)
+    if bad.size == 0:
+        return "equal"
+    i = tuple(bad[0])
+    return f"{len(bad)} diffs, first at {i}: got {a[i]} want {b[i]}"
+
+
+@pytest.mark.parametrize("idx", range(len(CASES)))
+def test_stage_case_fused(idx):
+    """Fused kernel, single head, per-stage dumps vs the reference's digests."""
+    row = CASES[idx]
+    case = row["case"]
+    q, k, v, mask = case_inputs(case)
+    L, d = q.shape
+    pf = ia.PFormat.UINT8X255 if case["p"] == 255 else ia.PFormat.INT8X127
+    cfg = ia.AttentionConfig(b=case["b"], c=case["c"], p_format=pf)
+    out, dbg = ia.int_attention_batched(q[None, None], k[None, None], v[None, None], mask=mask,
+                                        cfg=cfg, debug=True)
+    ref = O.int_attention(q, k, v, b=case["b"], c=case["c"], mask=mask, p_scale=case["p"])
+    assert digest(ref) == row["digests"]["out"]  # oracle pinned to the reference
+    if d <= 256:
+        qh = dbg["qhat"][0, :, :d].cpu().numpy()
+        assert digest(qh) == row["digests"]["qh"], _first_diff(qh, O.quantize_tensor(q)[0])
+        assert dbg["q_scales"].cpu().numpy()[0] == f32(row["sq"])
+        assert dbg["k_scales"].cpu().numpy()[0] == f32(row["sk"])
+        assert dbg["v_scales"].cpu().numpy()[0] == f32(row["sv"])
+        logits = dbg["logits"][0].cpu().numpy()
+        want_logits = O.matmul_s8(O.quantize_tensor(q)[0], O.quantize_tensor(k)[0])
+        if mask is None:
+            assert digest(logits) == row["digests"]["logits"], _first_diff(logits, want_logits)
+        else:  # the kernel only computes key tiles it needs (causal); compare where computed
+            keep = ~np.triu(np.ones((L, L), bool), 1) if case["mask"] == "causal" else np.ones((L, L), bool)
+            assert np.array_equal(logits[keep], want_logits[keep]), _first_diff(logits[keep], want_logits[keep])
+        prob = dbg["prob"][0].cpu().numpy()
+        want_p = O.index_softmax(want_logits, row["c_int"], np.array(row["lut"], np.uint8),
+                                 mask=mask, p_scale=case["p"])
+        assert digest(prob.view(np.int8) if case["p"] == 127 else prob) == row["digests"]["prob"], \
+            _first_diff(prob, want_p)
+        acc = dbg["acc"][0, :, :d].cpu().numpy()
+        assert digest(acc) == row["digests"]["acc"], _first_diff(acc, O.gemm_pv(want_p, O.quantize_tensor(v)[0]))
+    got = out[0, 0]
+    assert digest(got) == row["digests"]["out"], _first_diff(got.view(np.uint32), ref.view(np.uint32))
+
+
+@pytest.mark.parametrize("idx", range(0, len(CASES), 3))
+def test_stage_case_api(idx):
+    """The drop-in stage operators, one by one, vs the reference digests."""
+    row = CASES[idx]
+    case = row["case"]
+    q, k, v, mask = case_inputs(case)
+    pf = ia.PFormat.UINT8X255 if case["p"] == 255 else ia.PFormat.INT8X127
+    qh, kh, vh = ia.quantize_symmetric(q), ia.quantize_symmetric(k), ia.quantize_symmetric(v)
+    assert digest(qh.values) == row["digests"]["qh"]
+    assert digest(kh.values) == row["digests"]["kh"]
+    assert digest(vh.values) == row["digests"]["vh"]
+    assert qh.scales[0] == f32(row["sq"])
+    lm = ia.gemm_qk(qh, kh)
+    assert digest(lm.values) == row["digests"]["logits"]
+    assert float(lm.alpha).hex() == row["alpha"]
+    ci = ia.compute_c_int(case["c"], q.shape[1], qh.scales[0], kh.scales[0])
+    assert ci.c_int == row["c_int"]
+    lut = ia.build_lut(case["b"], case["c"])
+    assert lut.entries.tolist() == row["lut"]
+    prob = ia.index_softmax(lm, ci, lut, mask=mask, p_format=pf)
+    assert digest(prob.values) == row["digests"]["prob"], _first_diff(
+        prob.values, O.index_softmax(lm.values, ci.c_int, lut.entries, mask, case["p"]))
+    acc = ia.gemm_pv(prob.values, vh)
+    assert digest(acc) == row["digests"]["acc"]
+    out, t = ia.int_attention(q, k, v, ia.AttentionConfig(b=case["b"], c=case["c"], p_format=pf,
+                                                          mask=mask))
+    assert digest(out) == row["digests"]["out"]
+    assert t.total_ns > 0
+
+
+def test_kats_gpu():
+    q = ia.quantize_symmetric(np.array([[1.0, -2.0], [0.5, 2.54]], np.float32))
+    assert q.values.tolist() == [[50, -100], [25, 127]]
+    z = ia.quantize_symmetric(np.zeros((3, 4), np.float32))
+    assert not z.values.any() and z.scales[0] == np.float32(np.float32(1e-12) / np.float32(127))
+    a = ia.QuantizedMatrix(np.array([[1, 2]], np.int8), np.array([0.05], np.float32),
+                           ia.QuantGranularity.per_tensor())
+    b = ia.QuantizedMatrix(np.array([[3, 4]], np.int8), np.array([0.04], np.float32),
+                           ia.QuantGranularity.per_tensor())
+    assert ia.gemm_qk(a, b).values.tolist() == [[11]]
+    assert ia.gemm_pv(np.array([[255]], np.uint8), np.array([[7, -3]], np.int8)).tolist() == [[1785, -765]]
+    lut = ia.build_lut(5, 6.6)
+    assert ia.index_softmax(np.array([[100, 100], [100, 100]], np.int32), 37335, lut).values.tolist() == [[128, 128], [128, 128]]
+    assert ia.index_softmax(np.array([[100, 40], [40, 100]], np.int32), 50, lut).values.tolist() == [[255, 0], [0, 255]]
+    assert ia.index_softmax(np.array([[7]], np.int32), 5, lut).values.tolist() == [[255]]
+    m = np.array([[False, True], [True, True]])
+    assert ia.index_softmax(np.array([[1, 2], [3, 4]], np.int32), 50, lut, mask=m).values.tolist() == [[255, 0], [0, 0]]
+    p = ia.index_softmax(np.array([[100, 100], [100, 40]], np.int32), 50, lut,
+                         p_format=ia.PFormat.INT8X127)
+    assert p.values.dtype == np.int8 and p.values.tolist() == [[64, 64], [127, 0]]
+    with pytest.raises(ValueError):
+        ia.quantize_symmetric(np.array([[1.0, np.nan]], np.float32))
+    with pytest.raises(ValueError):
+        ia.int_attention(np.zeros((4, 3), np.float32), np.zeros((4, 3), np.float32),
+                         np.array([[np.inf, 0, 0]] * 4, np.float32))
+
+
+def test_gemm_random_shapes():
+    """SPEC acceptance 1: integer GEMMs vs a 64-bit triple loop, random shapes."""
+    rng = np.random.default_rng(7)
+    for _ in range(40):
+        m, n, kd = (int(x) for x in rng.integers(1, 300, size=3))
+        a = rng.integers(-127, 128, size=(m, kd)).astype(np.int8)
+        b = rng.integers(-127, 128, size=(n, kd)).astype(np.int8)
+        assert np.array_equal(ia.matmul_int8(a, b), a.astype(np.int64) @ b.astype(np.int64).T)
+        p = rng.integers(0, 256, size=(m, m)).astype(np.uint8)
+        vv = rng.integers(-127, 128, size=(m, kd)).astype(np.int8)
+        assert np.array_equal(ia.gemm_pv(p, vv), p.astype(np.int64) @ vv.astype(np.int64))
+
+
+def test_granularities():
+    rng = np.random.default_rng(3)
+    x = rng.standard_normal((64, 48), dtype=np.float32)
+    for g in (ia.QuantGranularity.per_row_group(16), ia.QuantGranularity.per_col_group(12)):
+        got = ia.quantize_symmetric(x, g)
+        if g.kind == "per_row_group":
+            want_v, want_s = O.quantize_groups(x, 4)
+        else:
+            xt = np.ascontiguousarray(x.reshape(64, 4, 12).transpose(1, 0, 2))
+            vv, want_s = O.quantize_groups(xt, 4)
+            want_v = vv.transpose(1, 0, 2).reshape(64, 48)
+        assert np.array_equal(got.values, want_v) and np.array_equal(got.scales, want_s)
+        deq = ia.dequantize(got)
+        assert np.array_equal(deq, (got.values.astype(np.float32) * got.scale_grid()).astype(np.float32))
+
+
+@pytest.mark.parametrize("L,d,causal,lens,H,Hkv,gran", [
+    (300, 64, True, None, 4, 2, "head"),
+    (517, 128, True, [517, 300, 129, 1], 2, 2, "head"),
+    (640, 128, False, None, 2, 1, "tensor"),
+    (257, 32, True, [257, 1], 3, 3, "head"),
+    (384, 256, True, None, 2, 2, "head"),
+    (130, 80, False, [100, 130], 2, 2, "tensor"),
+    (200, 300, True, None, 2, 1, "head"),
+])
+def test_batched_vs_oracle(L, d, causal, lens, H, Hkv, gran):
+    B = 1 if lens is None else len(lens)
+    rng = np.random.default_rng(L + d)
+    q = rng.standard_normal((B, H, L, d), dtype=np.float32)
+    k = rng.standard_normal((B, Hkv, L, d), dtype=np.float32) * np.float32(2.0)
+    v = rng.standard_normal((B, Hkv, L, d), dtype=np.float32)
+    sl = None if lens is None else np.array(lens, np.int32)
+    if sl is not None:
+        for b, n in enumerate(sl):
+            q[b, :, n:] = 0
+            k[b, :, n:] = 0
+            v[b, :, n:] = 0
+    got = ia.int_attention_batched(q, k, v, causal=causal, seq_lens=sl, scale_granularity=gran)
+    want, _ = O.attention_batched(q, k, v, causal=causal, seq_lens=sl, scale_granularity=gran)
+    assert np.array_equal(got.view(np.uint32), want.view(np.uint32)), _first_diff(got, want)
+
+
+def test_dense_mask_batched():
+    rng = np.random.default_rng(11)
+    L, d = 333, 64
+    q = rng.standard_normal((2, 2, L, d), dtype=np.float32)
+    k = rng.standard_normal((2, 2, L, d), dtype=np.float32)
+    v = rng.standard_normal((2, 2, L, d), dtype=np.float32)
+    mask = rng.random((L, L)) < 0.5
+    mask[5, :] = True
+    got = ia.int_attention_batched(q, k, v, mask=mask, causal=True)
+    want, _ = O.attention_batched(q, k, v, mask=mask, causal=True)
+    assert np.array_equal(got.view(np.uint32), want.view(np.uint32)), _first_diff(got, want)
+    assert not got[:, :, 5].any()
+
+
+def test_torch_inputs_stay_on_device():
+    rng = np.random.default_rng(5)
+    q = rng.standard_normal((1, 2, 256, 64), dtype=np.float32)
+    qt = torch.from_numpy(q).cuda()
+    out = ia.int_attention_batched(qt, qt, qt, causal=True)
+    assert out.is_cuda
+    want, _ = O.attention_batched(q, q, q, causal=True)
+    assert np.array_equal(out.cpu().numpy().view(np.uint32), want.view(np.uint32))
