@@ -38,11 +38,8 @@ namespace ia {
 
 constexpr int BM = 128;  // query rows per tile (= TMEM lanes)
 constexpr int BN = 128;  // keys per tile
-constexpr int NKST = 3;  // K smem stages
 constexpr int NVST = 2;  // V^T smem stages
-constexpr int NTHREADS = 384;
 constexpr uint32_t TMEM_COLS = 512;
-constexpr uint32_t O_COL = 256;
 
 struct AttnDev {
   float* out;
@@ -59,6 +56,12 @@ struct AttnDev {
 
 template <int DP>
 struct Cfg {
+  // softmax warpgroups == TMEM S buffers (one 128-column buffer each); O sits after them.
+  // Each warpgroup also owns one smem P^ tile.
+  static constexpr int NWG = DP <= 128 ? 3 : 2;
+  static constexpr int NKST = DP <= 128 ? 3 : 2;  // K smem stages
+  static constexpr int NTHREADS = 128 + 128 * NWG;
+  static constexpr uint32_t O_COL = 128 * NWG;
   static constexpr int SW = DP >= 128 ? 128 : DP;  // swizzle span (bytes) of Q/K rows
   static constexpr int NSUB = DP / SW;              // 128-row sub-blocks per Q/K tile
   static constexpr uint32_t LAYOUT = SW == 128 ? 2u : (SW == 64 ? 4u : 6u);
@@ -70,14 +73,22 @@ struct Cfg {
   static constexpr int OFF_Q = 0;
   static constexpr int OFF_K = Q_BYTES;
   static constexpr int OFF_V = OFF_K + NKST * K_BYTES;
-  static constexpr int OFF_TAB = OFF_V + NVST * V_BYTES;
+  static constexpr int P_BYTES = BM * BN;  // u8 P^ tile, K-major SWIZZLE_128B (A of P.V)
+  static constexpr int OFF_P = OFF_V + NVST * V_BYTES;
+  static constexpr int OFF_TAB = OFF_P + NWG * P_BYTES;
   static constexpr int KSTEPS = DP / 32;
+  static constexpr int STAGE_PITCH = DP + 1;  // f32 epilogue staging row pitch (words, conflict-free)
+  static_assert(OFF_TAB >= BM * STAGE_PITCH * 4, "epilogue staging must fit in Q/K/V stages");
 };
 
-__host__ __device__ constexpr size_t attn_smem_bytes(int dp, int nlut) {
-  return 1024 /* alignment slack */ + (size_t)(dp * 128) * (1 + NKST + NVST) +
-         (size_t)nlut * 512 /* row tables */ + 1024 /* lut */ + 2048 /* row exchange */ +
-         256 /* barriers + tmem slot */;
+// Row tables: u32 [nlut][128] (conflict-free gathers) for nlut <= 64, else u8.
+__host__ __device__ constexpr bool wide_tab(int nlut) { return nlut <= 64; }
+
+template <int DP>
+constexpr size_t attn_smem_bytes(int nlut) {
+  return 1024 /* alignment slack */ + (size_t)Cfg<DP>::OFF_TAB +
+         (size_t)nlut * (wide_tab(nlut) ? 512 : 128) /* row tables */ +
+         2 * 3 * 512 /* row exchange */ + 256 /* barriers + tmem slot */;
 }
 
 // Masked-key bits for one 32-key chunk starting at j0 for query row i
@@ -89,31 +100,44 @@ __device__ __forceinline__ uint32_t chunk_mask(const AttnDev& p, int i, int j0, 
   return mb;
 }
 
+__device__ __forceinline__ uint32_t lds_u8(uint32_t addr) {
+  uint32_t v;
+  asm("ld.shared.u8 %0, [%1];" : "=r"(v) : "r"(addr));
+  return v;
+}
+__device__ __forceinline__ uint32_t lds_u32(uint32_t addr) {
+  uint32_t v;
+  asm("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(addr));
+  return v;
+}
+
 template <int DP, bool DEBUG>
-__global__ void __launch_bounds__(NTHREADS, 1)
+__global__ void __launch_bounds__(Cfg<DP>::NTHREADS, 1)
     attn_fwd_kernel(const __grid_constant__ CUtensorMap tmq,
                     const __grid_constant__ CUtensorMap tmk,
                     const __grid_constant__ CUtensorMap tmv, const __grid_constant__ AttnDev p) {
   using C = Cfg<DP>;
+  constexpr int NWG = C::NWG;
   extern __shared__ uint8_t smem_raw[];
+  __shared__ uint8_t lut8[256];  // static: LDS.U8 [idx + const] in the pass-2 gather
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~uintptr_t(1023));
   const int nlut = p.nlut;
-  uint32_t* tab = reinterpret_cast<uint32_t*>(smem + C::OFF_TAB);  // [nlut][128] row tables
-  uint32_t* lut_s = tab + nlut * 128;                               // [256]
-  int32_t* xmax = reinterpret_cast<int32_t*>(lut_s + 256);          // [2][128]
-  uint32_t* xsum = reinterpret_cast<uint32_t*>(xmax + 256);         // [2][128]
-  uint64_t* bars = reinterpret_cast<uint64_t*>(xsum + 256);
+  const bool wtab = wide_tab(nlut);
+  uint8_t* tab = smem + C::OFF_TAB;  // row tables [nlut][128], u32 (wide) or u8 entries
+  int32_t* xmax = reinterpret_cast<int32_t*>(tab + nlut * (wtab ? 512 : 128));  // [NWG][128]
+  uint32_t* xsum = reinterpret_cast<uint32_t*>(xmax + 3 * 128);     // [NWG][128]
+  uint64_t* bars = reinterpret_cast<uint64_t*>(xsum + 3 * 128);
   uint64_t* q_full = bars;
   uint64_t* k_full = q_full + 1;
-  uint64_t* k_empty = k_full + NKST;
-  uint64_t* v_full = k_empty + NKST;
+  uint64_t* k_empty = k_full + C::NKST;
+  uint64_t* v_full = k_empty + C::NKST;
   uint64_t* v_empty = v_full + NVST;
-  uint64_t* s_full = v_empty + NVST;      // [2] MMA -> softmax (QK^T landed)
-  uint64_t* s_free_sm = s_full + 2;       // [2] softmax -> MMA (S read, passes 1-2)
-  uint64_t* s_free_mma = s_free_sm + 2;   // [2] MMA -> MMA (P.V consumed P^, pass 3)
-  uint64_t* p_full = s_free_mma + 2;      // [2] softmax -> MMA (P^ in TMEM)
-  uint64_t* o_full = p_full + 2;          // MMA -> epilogue
+  uint64_t* s_full = v_empty + NVST;  // [NWG] MMA -> softmax (QK^T landed in S[w])
+  uint64_t* s_free = s_full + NWG;    // [NWG] softmax -> MMA (S[w] fully read)
+  uint64_t* p_full = s_free + NWG;    // [NWG] softmax -> MMA (P^ tile w written to smem)
+  uint64_t* p_free = p_full + NWG;    // [NWG] MMA -> softmax (P.V finished reading P^ tile w)
+  uint64_t* o_full = p_free + NWG;    // MMA -> epilogue
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(o_full + 1);
 
   const int BH = p.B * p.H;
@@ -128,25 +152,25 @@ __global__ void __launch_bounds__(NTHREADS, 1)
   if (q0 >= len) {  // the whole query tile is padding: +0.0 rows (pipeline contract)
     const int rows = min(BM, p.L - q0);
     float* o = p.out + ((size_t)bh * p.L + q0) * p.d;
-    for (int t = threadIdx.x; t < rows * p.d; t += NTHREADS) o[t] = 0.0f;
+    for (int t = threadIdx.x; t < rows * p.d; t += C::NTHREADS) o[t] = 0.0f;
     return;
   }
   const int key_end = p.causal ? min(q0 + BM, len) : len;
   const int n_kt = (key_end + BN - 1) / BN;
-  const bool resident = n_kt <= 2;
+  const bool resident = n_kt <= NWG;  // every logit tile fits its own TMEM buffer
 
   if (warp == 0 && lane == 0) {
     prefetch_tmap(&tmq);
     prefetch_tmap(&tmk);
     prefetch_tmap(&tmv);
     mbar_init(q_full, 1);
-    for (int s = 0; s < NKST; ++s) { mbar_init(k_full + s, 1); mbar_init(k_empty + s, 1); }
+    for (int s = 0; s < C::NKST; ++s) { mbar_init(k_full + s, 1); mbar_init(k_empty + s, 1); }
     for (int s = 0; s < NVST; ++s) { mbar_init(v_full + s, 1); mbar_init(v_empty + s, 1); }
-    for (int w = 0; w < 2; ++w) {
+    for (int w = 0; w < NWG; ++w) {
       mbar_init(s_full + w, 1);
-      mbar_init(s_free_sm + w, 128);
-      mbar_init(s_free_mma + w, 1);
+      mbar_init(s_free + w, 128);
       mbar_init(p_full + w, 128);
+      mbar_init(p_free + w, 1);
     }
     mbar_init(o_full, 1);
     fence_mbar_init();
@@ -155,7 +179,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     tmem_alloc(tmem_slot, TMEM_COLS);
     tmem_relinquish();
   }
-  for (int t = threadIdx.x; t < 256; t += NTHREADS) lut_s[t] = t < nlut ? p.lut[t] : 0u;
+  for (int t = threadIdx.x; t < 256; t += C::NTHREADS) lut8[t] = t < nlut ? p.lut[t] : 0;
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
@@ -167,40 +191,50 @@ __global__ void __launch_bounds__(NTHREADS, 1)
       mbar_expect_tx(q_full, C::Q_BYTES);
       for (int s = 0; s < C::NSUB; ++s)
         tma_load_3d(smem + C::OFF_Q + s * C::SUB_BYTES, &tmq, q_full, s * C::SW, q0, bh);
+      // Load order == the MMA warp's consumption order (see below), so the K and
+      // V^T rings can never block each other.
       int ks = 0, kph = 0, vs = 0, vph = 0;
-      const int npass = resident ? 1 : 3;
-      for (int pass = 0; pass < npass; ++pass) {
-        const bool with_v = pass == npass - 1;
+      auto load_k = [&](int n) {
+        mbar_wait(k_empty + ks, kph ^ 1);
+        mbar_expect_tx(k_full + ks, C::K_BYTES);
+        for (int s = 0; s < C::NSUB; ++s)
+          tma_load_3d(smem + C::OFF_K + ks * C::K_BYTES + s * C::SUB_BYTES, &tmk, k_full + ks,
+                      s * C::SW, n * BN, kvh);
+        if (++ks == C::NKST) { ks = 0; kph ^= 1; }
+      };
+      auto load_v = [&](int n) {
+        mbar_wait(v_empty + vs, vph ^ 1);
+        mbar_expect_tx(v_full + vs, C::V_BYTES);
+        tma_load_3d(smem + C::OFF_V + vs * C::V_BYTES, &tmv, v_full + vs, n * BN, 0, kvh);
+        if (++vs == NVST) { vs = 0; vph ^= 1; }
+      };
+      if (resident) {
+        for (int n = 0; n < n_kt; ++n) load_k(n);
+        for (int n = 0; n < n_kt; ++n) load_v(n);
+      } else {
+        for (int pass = 0; pass < 2; ++pass)
+          for (int n = 0; n < n_kt; ++n) load_k(n);
+        for (int n = 0; n < NWG && n < n_kt; ++n) load_k(n);
         for (int n = 0; n < n_kt; ++n) {
-          mbar_wait(k_empty + ks, kph ^ 1);
-          mbar_expect_tx(k_full + ks, C::K_BYTES);
-          for (int s = 0; s < C::NSUB; ++s)
-            tma_load_3d(smem + C::OFF_K + ks * C::K_BYTES + s * C::SUB_BYTES, &tmk, k_full + ks,
-                        s * C::SW, n * BN, kvh);
-          if (++ks == NKST) { ks = 0; kph ^= 1; }
-          if (with_v) {
-            mbar_wait(v_empty + vs, vph ^ 1);
-            mbar_expect_tx(v_full + vs, C::V_BYTES);
-            tma_load_3d(smem + C::OFF_V + vs * C::V_BYTES, &tmv, v_full + vs, n * BN, 0, kvh);
-            if (++vs == NVST) { vs = 0; vph ^= 1; }
-          }
+          if (n + NWG < n_kt) load_k(n + NWG);
+          load_v(n);
         }
       }
     }
   } else if (warp == 1) {
     // ------------------------------------------------------------ MMA issuer
+    // Tile n of every pass lives in TMEM buffer / warpgroup w = n % NWG.
     if (lane == 0) {
       constexpr uint32_t idq = idesc_i8(BM, BN, true, true);   // s8 x s8 -> s32
       constexpr uint32_t idv = idesc_i8(BM, DP, false, true);  // u8 x s8 -> s32
       const uint32_t sq = smem_u32(smem + C::OFF_Q);
       mbar_wait(q_full, 0);
       int ks = 0, kph = 0, vs = 0, vph = 0;
-      int prev[2] = {0, 0};  // how S[w]'s last occupant is released: 0 none, 1 softmax, 2 P.V
-      uint32_t c_sm[2] = {0, 0}, c_mma[2] = {0, 0}, c_p[2] = {0, 0};
-      auto issue_qk = [&](int n, int release) {
-        const int w = n & 1;
-        if (prev[w] == 1) { mbar_wait(s_free_sm + w, c_sm[w] & 1); ++c_sm[w]; }
-        else if (prev[w] == 2) { mbar_wait(s_free_mma + w, c_mma[w] & 1); ++c_mma[w]; }
+      uint32_t used = 0, c_s = 0, c_p = 0;  // per-buffer: occupied bit, s_free / p_full phases
+      auto issue_qk = [&](int n) {
+        const int w = n % NWG;
+        if ((used >> w) & 1u) { mbar_wait(s_free + w, (c_s >> w) & 1u); c_s ^= 1u << w; }
+        used |= 1u << w;
         mbar_wait(k_full + ks, kph);
         tc_fence_after();
         const uint32_t sk = smem_u32(smem + C::OFF_K + ks * C::K_BYTES);
@@ -212,34 +246,35 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         }
         tc_commit(k_empty + ks);
         tc_commit(s_full + w);
-        if (++ks == NKST) { ks = 0; kph ^= 1; }
-        prev[w] = release;
+        if (++ks == C::NKST) { ks = 0; kph ^= 1; }
       };
       auto issue_pv = [&](int n) {
-        const int w = n & 1;
-        mbar_wait(p_full + w, c_p[w] & 1);
-        ++c_p[w];
+        const int w = n % NWG;
+        mbar_wait(p_full + w, (c_p >> w) & 1u);
+        c_p ^= 1u << w;
         mbar_wait(v_full + vs, vph);
         tc_fence_after();
+        const uint32_t sp = smem_u32(smem + C::OFF_P + w * C::P_BYTES);
         const uint32_t sv = smem_u32(smem + C::OFF_V + vs * C::V_BYTES);
 #pragma unroll
         for (int kk = 0; kk < BN / 32; ++kk)
-          mma_i8_ts(tmem + O_COL, tmem + w * 128 + kk * 8, sdesc(sv + kk * 32, 1024, 2u), idv,
-                    (n > 0 || kk > 0) ? 1u : 0u);
+          mma_i8_ss(tmem + C::O_COL, sdesc(sp + kk * 32, 1024, 2u), sdesc(sv + kk * 32, 1024, 2u),
+                    idv, (n > 0 || kk > 0) ? 1u : 0u);
         tc_commit(v_empty + vs);
-        tc_commit(s_free_mma + w);
+        tc_commit(p_free + w);
         if (++vs == NVST) { vs = 0; vph ^= 1; }
       };
       if (!resident) {
         for (int pass = 0; pass < 2; ++pass)
-          for (int n = 0; n < n_kt; ++n) issue_qk(n, 1);
+          for (int n = 0; n < n_kt; ++n) issue_qk(n);
+        // pass 3: QK^T(n + NWG) only needs S[w] read back, so it runs ahead of P.V(n)
+        for (int n = 0; n < NWG && n < n_kt; ++n) issue_qk(n);
         for (int n = 0; n < n_kt; ++n) {
-          issue_qk(n, 2);
-          if (n >= 1) issue_pv(n - 1);
+          if (n + NWG < n_kt) issue_qk(n + NWG);
+          issue_pv(n);
         }
-        issue_pv(n_kt - 1);
       } else {
-        for (int n = 0; n < n_kt; ++n) issue_qk(n, 0);
+        for (int n = 0; n < n_kt; ++n) issue_qk(n);
         for (int n = 0; n < n_kt; ++n) issue_pv(n);
       }
       tc_commit(o_full);
@@ -247,7 +282,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
   } else if (warp >= 4) {
     // ------------------------------------------------------------ IndexSoftmax warpgroups
     const int wg = (warp - 4) >> 2;
-    const int quad = warp & 3;             // TMEM lane quadrant accessible to this warp
+    const int quad = warp & 3;  // TMEM lane quadrant accessible to this warp
     const int row = quad * 32 + lane;
     const int i = q0 + row;
     const bool row_valid = i < len;
@@ -255,164 +290,220 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     const uint32_t s_base = tmem + t_lane + (uint32_t)(wg * 128);
     const int lim = p.causal ? min(i, len - 1) : len - 1;  // last unmasked key of this row
     const ia_head_params hp = p.params[bh];
-    uint32_t s_cnt = 0;
+    const uint32_t k = (uint32_t)(nlut - 1);
+    constexpr int NWT = 128 * NWG;  // softmax threads
+    uint32_t s_ph = 0;              // phase of s_full[wg]
 
+    // Each tile is read from TMEM in two 64-column batches (two x32 loads in
+    // flight per wait); S[w] is handed back to the MMA warp right after the last
+    // load of the tile, in every pass.
     // ---- pass 1: row max over unmasked keys (softmax.py:139-143, :174-179)
     int32_t mx = INT_MIN;
-    for (int n = wg; n < n_kt; n += 2) {
-      mbar_wait(s_full + wg, s_cnt & 1);
-      ++s_cnt;
+    for (int n = wg; n < n_kt; n += NWG) {
+      mbar_wait(s_full + wg, s_ph);
+      s_ph ^= 1u;
       tc_fence_after();
 #pragma unroll 1
-      for (int c = 0; c < BN / 32; ++c) {
-        uint32_t v[32];
-        tmem_ld32(s_base + c * 32, v);
-        const int j0 = n * BN + c * 32;
+      for (int hb = 0; hb < BN / 64; ++hb) {
+        uint32_t va[32], vb[32];
+        tmem_ld64(s_base + hb * 64, va, vb);
+        if (hb == BN / 64 - 1 && !resident) {
+          tc_fence_before();
+          mbar_arrive(s_free + wg);
+        }
+        const int j0 = n * BN + hb * 64;
         if (DEBUG && p.dbg_logits && i < p.L) {
-          for (int e = 0; e < 32; ++e)
-            if (j0 + e < p.L) p.dbg_logits[((size_t)bh * p.L + i) * p.L + j0 + e] = (int32_t)v[e];
+#pragma unroll
+          for (int e = 0; e < 32; ++e) {
+            int32_t* dl = p.dbg_logits + ((size_t)bh * p.L + i) * p.L + j0;
+            if (j0 + e < p.L) dl[e] = (int32_t)va[e];
+            if (j0 + 32 + e < p.L) dl[32 + e] = (int32_t)vb[e];
+          }
         }
         if (!row_valid) continue;
-        const uint32_t mb = chunk_mask(p, i, j0, lim);
-        if (mb == 0) {
+        const uint32_t ma = chunk_mask(p, i, j0, lim), mbb = chunk_mask(p, i, j0 + 32, lim);
+        if ((ma | mbb) == 0) {
 #pragma unroll
-          for (int e = 0; e < 32; ++e) mx = max(mx, (int32_t)v[e]);
+          for (int e = 0; e < 32; e += 2)
+            mx = max(mx, max(max((int32_t)va[e], (int32_t)va[e + 1]),
+                             max((int32_t)vb[e], (int32_t)vb[e + 1])));
         } else {
 #pragma unroll
-          for (int e = 0; e < 32; ++e)
-            if (!((mb >> e) & 1u)) mx = max(mx, (int32_t)v[e]);
+          for (int e = 0; e < 32; ++e) {
+            if (!((ma >> e) & 1u)) mx = max(mx, (int32_t)va[e]);
+            if (!((mbb >> e) & 1u)) mx = max(mx, (int32_t)vb[e]);
+          }
         }
       }
-      tc_fence_before();
-      if (!resident) mbar_arrive(s_free_sm + wg);
     }
     xmax[wg * 128 + row] = mx;
-    named_bar_sync(1, 256);
-    int32_t m = max(xmax[row], xmax[128 + row]);
+    named_bar_sync(1, NWT);
+    int32_t m = xmax[row];
+#pragma unroll
+    for (int w = 1; w < NWG; ++w) m = max(m, xmax[w * 128 + row]);
     const bool dead = (m == INT_MIN);  // fully masked row: all-zero P^ (softmax.py:181-184)
     if (dead) m = 0;
+    const bool fast = hp.use32 != 0;
+    IdxMap im;
+    im.init(m, hp, k);
 
     // ---- pass 2: idx, e = lut[idx], S = sum e (softmax.py:144-155)
-    const int64_t k64 = nlut - 1;
-    IdxMap im;
-    im.k2 = 2u * (uint32_t)k64;
-    im.magic = hp.magic;
-    im.shift = hp.shift;
-    im.lo = hp.use32 ? idx_lo(m, hp.c_eff) : 0;
-    im.base = (uint32_t)m * im.k2 + (uint32_t)hp.c_eff;
-    const bool fast = hp.use32 != 0;
     uint32_t S = 0;
-    for (int n = wg; n < n_kt; n += 2) {
+    for (int n = wg; n < n_kt; n += NWG) {
       if (!resident) {
-        mbar_wait(s_full + wg, s_cnt & 1);
-        ++s_cnt;
+        mbar_wait(s_full + wg, s_ph);
+        s_ph ^= 1u;
       }
       tc_fence_after();
 #pragma unroll 1
-      for (int c = 0; c < BN / 32; ++c) {
-        uint32_t v[32];
-        tmem_ld32(s_base + c * 32, v);
+      for (int hb = 0; hb < BN / 64; ++hb) {
+        uint32_t va[32], vb[32];
+        tmem_ld64(s_base + hb * 64, va, vb);
+        if (hb == BN / 64 - 1 && !resident) {
+          tc_fence_before();
+          mbar_arrive(s_free + wg);
+        }
         if (!row_valid || dead) continue;
-        const int j0 = n * BN + c * 32;
-        const uint32_t mb = chunk_mask(p, i, j0, lim);
-        if (fast) {
-          if (mb == 0) {
+        const int j0 = n * BN + hb * 64;
+        const uint32_t ma = chunk_mask(p, i, j0, lim), mbb = chunk_mask(p, i, j0 + 32, lim);
+        if (fast && (ma | mbb) == 0) {
 #pragma unroll
-            for (int e = 0; e < 32; ++e) S += lut_s[im.idx((int32_t)v[e])];
-          } else {
-#pragma unroll
-            for (int e = 0; e < 32; ++e)
-              S += lut_s[((mb >> e) & 1u) ? (uint32_t)k64 : im.idx((int32_t)v[e])];
-          }
-        } else {
           for (int e = 0; e < 32; ++e)
-            S += lut_s[((mb >> e) & 1u) ? (uint32_t)k64 : idx_slow(m, (int32_t)v[e], hp.c_eff, k64)];
+            S += (uint32_t)lut8[im.idx((int32_t)va[e])] + (uint32_t)lut8[im.idx((int32_t)vb[e])];
+        } else {
+#pragma unroll
+          for (int e = 0; e < 32; ++e) {
+            if (!((ma >> e) & 1u))
+              S += lut8[fast ? im.idx((int32_t)va[e]) : idx_slow(m, (int32_t)va[e], hp.c_eff, k)];
+            if (!((mbb >> e) & 1u))
+              S += lut8[fast ? im.idx((int32_t)vb[e]) : idx_slow(m, (int32_t)vb[e], hp.c_eff, k)];
+          }
         }
       }
-      tc_fence_before();
-      if (!resident) mbar_arrive(s_free_sm + wg);
     }
     xsum[wg * 128 + row] = S;
-    named_bar_sync(1, 256);
-    S = xsum[row] + xsum[128 + row];
+    named_bar_sync(1, NWT);
+    S = xsum[row];
+#pragma unroll
+    for (int w = 1; w < NWG; ++w) S += xsum[w * 128 + row];
     // per-row normalisation table (softmax.py:157-160): (2*scale*lut[t] + S) // (2S)
     {
-      const int half = nlut >> 1;
       const uint32_t two_s = 2u * S;
-      for (int t = wg * half; t < (wg + 1) * half; ++t)
-        tab[t * 128 + row] = S ? ((uint32_t)p.scale_x2 * lut_s[t] + S) / two_s : 0u;
+      for (int t = wg; t < nlut; t += NWG) {
+        const uint32_t pv = S ? ((uint32_t)p.scale_x2 * lut8[t] + S) / two_s : 0u;
+        if (wtab) reinterpret_cast<uint32_t*>(tab)[t * 128 + row] = pv;
+        else tab[t * 128 + row] = (uint8_t)pv;
+      }
     }
-    named_bar_sync(1, 256);
-    const uint32_t* trow = tab + row;
+    named_bar_sync(1, NWT);
+    // entry idx of this row: wide: tab_row + idx * 512 (u32), else tab_row + idx * 128 (u8)
+    const uint32_t tab_row = smem_u32(tab) + (uint32_t)row * (wtab ? 4u : 1u);
+    const uint32_t tab_sh = wtab ? 9u : 7u;
+    // this thread's row of its warpgroup's P^ tile (K-major, 128B swizzle: 16-byte
+    // unit x of row r lives at unit x ^ (r % 8))
+    const uint32_t p_row = smem_u32(smem + C::OFF_P + wg * C::P_BYTES) + (uint32_t)row * 128;
+    const uint32_t p_xor = (uint32_t)(row & 7);
+    uint32_t pf_ph = 0;
 
-    // ---- pass 3: P^ = rowtab[idx] -> TMEM (in place over S[w]) -> P.V (softmax.py:161-162)
-    for (int n = wg; n < n_kt; n += 2) {
+    // ---- pass 3: P^ = rowtab[idx] -> smem -> P.V MMA (softmax.py:161-162)
+    for (int n = wg; n < n_kt; n += NWG) {
       if (!resident) {
-        mbar_wait(s_full + wg, s_cnt & 1);
-        ++s_cnt;
+        mbar_wait(s_full + wg, s_ph);
+        s_ph ^= 1u;
       }
       tc_fence_after();
+      mbar_wait(p_free + wg, pf_ph ^ 1u);  // previous P.V done with this P^ tile
+      pf_ph ^= 1u;
 #pragma unroll 1
-      for (int c = 0; c < BN / 32; ++c) {
-        uint32_t v[32];
-        tmem_ld32(s_base + c * 32, v);
-        uint32_t pk[8];
+      for (int hb = 0; hb < BN / 64; ++hb) {
+        uint32_t va[32], vb[32];
+        tmem_ld64(s_base + hb * 64, va, vb);
+        if (hb == BN / 64 - 1 && !resident) {
+          tc_fence_before();
+          mbar_arrive(s_free + wg);
+        }
+        const int j0 = n * BN + hb * 64;
+        uint32_t pk[16];
 #pragma unroll
-        for (int q = 0; q < 8; ++q) pk[q] = 0u;
-        const int j0 = n * BN + c * 32;
+        for (int q = 0; q < 16; ++q) pk[q] = 0u;
         if (row_valid && !dead) {
-          const uint32_t mb = chunk_mask(p, i, j0, lim);
-          if (fast) {
-            if (mb == 0) {
+          const uint32_t ma = chunk_mask(p, i, j0, lim), mbb = chunk_mask(p, i, j0 + 32, lim);
+          if (fast && wtab && (ma | mbb) == 0) {
 #pragma unroll
-              for (int e = 0; e < 32; ++e)
-                pk[e >> 2] |= trow[im.idx((int32_t)v[e]) * 128] << (8 * (e & 3));
-            } else {
-#pragma unroll
-              for (int e = 0; e < 32; ++e) {
-                const uint32_t x = ((mb >> e) & 1u) ? (uint32_t)k64 : im.idx((int32_t)v[e]);
-                pk[e >> 2] |= trow[x * 128] << (8 * (e & 3));
-              }
+            for (int q = 0; q < 16; ++q) {
+              const uint32_t* v4 = q < 8 ? &va[4 * q] : &vb[4 * (q - 8)];
+              const uint32_t p0 = lds_u32(tab_row + (im.idx((int32_t)v4[0]) << 9));
+              const uint32_t p1 = lds_u32(tab_row + (im.idx((int32_t)v4[1]) << 9));
+              const uint32_t p2 = lds_u32(tab_row + (im.idx((int32_t)v4[2]) << 9));
+              const uint32_t p3 = lds_u32(tab_row + (im.idx((int32_t)v4[3]) << 9));
+              pk[q] = __byte_perm(__byte_perm(p0, p1, 0x0040), __byte_perm(p2, p3, 0x0040), 0x5410);
             }
           } else {
+#pragma unroll
             for (int e = 0; e < 32; ++e) {
-              const uint32_t x = ((mb >> e) & 1u) ? (uint32_t)k64 : idx_slow(m, (int32_t)v[e], hp.c_eff, k64);
-              pk[e >> 2] |= trow[x * 128] << (8 * (e & 3));
+              const uint32_t xa = ((ma >> e) & 1u) ? k
+                                  : fast ? im.idx((int32_t)va[e])
+                                         : idx_slow(m, (int32_t)va[e], hp.c_eff, k);
+              const uint32_t xb = ((mbb >> e) & 1u) ? k
+                                  : fast ? im.idx((int32_t)vb[e])
+                                         : idx_slow(m, (int32_t)vb[e], hp.c_eff, k);
+              const uint32_t aa = tab_row + (xa << tab_sh), ab = tab_row + (xb << tab_sh);
+              pk[e >> 2] |= (wtab ? lds_u32(aa) : lds_u8(aa)) << (8 * (e & 3));
+              pk[8 + (e >> 2)] |= (wtab ? lds_u32(ab) : lds_u8(ab)) << (8 * (e & 3));
             }
           }
         }
         if (DEBUG && p.dbg_prob && i < p.L) {
-          for (int e = 0; e < 32; ++e)
+#pragma unroll
+          for (int e = 0; e < 64; ++e)
             if (j0 + e < p.L)
               p.dbg_prob[((size_t)bh * p.L + i) * p.L + j0 + e] = (uint8_t)(pk[e >> 2] >> (8 * (e & 3)));
         }
-        tmem_st8(s_base + c * 8, pk);
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {  // 16-byte units 4*hb + u of this row
+          const uint32_t x = (uint32_t)(4 * hb + u);
+          sts128(p_row + ((x ^ p_xor) << 4), pk[4 * u], pk[4 * u + 1], pk[4 * u + 2], pk[4 * u + 3]);
+        }
       }
-      tmem_st_wait();
-      tc_fence_before();
+      fence_proxy_async_smem();
       mbar_arrive(p_full + wg);
     }
 
     // ---- epilogue: out = f32(acc) * f32(s_v / scale) (pipeline.py:250-252)
+    // TMEM -> registers -> smem staging (all TMA/MMA traffic has drained once
+    // o_full fires) -> coalesced row-contiguous global stores.
     mbar_wait(o_full, 0);
     tc_fence_after();
-    constexpr int HALF = DP / 2;
+    float* stage = reinterpret_cast<float*>(smem);
+    const float osc = hp.out_scale;
 #pragma unroll 1
-    for (int c0 = wg * HALF; c0 < (wg + 1) * HALF; c0 += 16) {
+    for (int c0 = wg * 16; c0 < DP; c0 += 16 * NWG) {
       uint32_t a[16];
-      tmem_ld16(tmem + t_lane + O_COL + c0, a);
-      if (i < p.L) {
-        float* orow = p.out + ((size_t)bh * p.L + i) * p.d;
+      tmem_ld16(tmem + t_lane + C::O_COL + c0, a);
 #pragma unroll
-        for (int e = 0; e < 16; ++e) {
-          const int col = c0 + e;
-          if (col < p.d)
-            orow[col] = row_valid ? __fmul_rn(__int2float_rn((int32_t)a[e]), hp.out_scale) : 0.0f;
-        }
-        if (DEBUG && p.dbg_acc) {
-          for (int e = 0; e < 16; ++e)
-            p.dbg_acc[((size_t)bh * p.L + i) * DP + c0 + e] = (int32_t)a[e];
-        }
+      for (int e = 0; e < 16; ++e)
+        stage[row * C::STAGE_PITCH + c0 + e] =
+            row_valid ? __fmul_rn(__int2float_rn((int32_t)a[e]), osc) : 0.0f;
+      if (DEBUG && p.dbg_acc && i < p.L) {
+        for (int e = 0; e < 16; ++e)
+          p.dbg_acc[((size_t)bh * p.L + i) * DP + c0 + e] = (int32_t)a[e];
+      }
+    }
+    named_bar_sync(1, NWT);
+    const int rows = min(BM, p.L - q0);
+    float* obase = p.out + ((size_t)bh * p.L + q0) * p.d;
+    const int tid = threadIdx.x - 128;
+    if ((p.d & 3) == 0) {
+      const int d4 = p.d >> 2;
+      for (int t = tid; t < rows * d4; t += NWT) {
+        const int r = t / d4, c4 = (t - r * d4) << 2;
+        const float* s4 = stage + r * C::STAGE_PITCH + c4;
+        *reinterpret_cast<float4*>(obase + (size_t)r * p.d + c4) = make_float4(s4[0], s4[1], s4[2], s4[3]);
+      }
+    } else {
+      for (int t = tid; t < rows * p.d; t += NWT) {
+        const int r = t / p.d, cc = t - r * p.d;
+        obase[(size_t)r * p.d + cc] = stage[r * C::STAGE_PITCH + cc];
       }
     }
   }
@@ -463,14 +554,14 @@ static int launch_attn(const ia_attn_args* a, cudaStream_t st) {
   dv.scale_x2 = 2 * a->p_scale;
   dv.n_qt = (int)((a->L + BM - 1) / BM);
   for (int t = 0; t < 256; ++t) dv.lut[t] = t < a->nlut ? a->lut[t] : 0;
-  size_t smem = attn_smem_bytes(DP, a->nlut);
+  size_t smem = attn_smem_bytes<DP>(a->nlut);
   if (smem < 120 * 1024) smem = 120 * 1024;  // one CTA per SM (it owns all 512 TMEM columns)
   auto kern = attn_fwd_kernel<DP, DEBUG>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return fail(IA_ERR_CUDA, "smem attribute: %s", cudaGetErrorString(e));
   const uint64_t grid = (uint64_t)dv.n_qt * BH;
   if (grid > 0x7fffffffull) return fail(IA_ERR_INVALID_ARGUMENT, "grid too large");
-  kern<<<(unsigned)grid, NTHREADS, smem, st>>>(tq, tk, tv, dv);
+  kern<<<(unsigned)grid, C::NTHREADS, smem, st>>>(tq, tk, tv, dv);
   return check_launch("attn_fwd_kernel");
 }
 

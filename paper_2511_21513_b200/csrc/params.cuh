@@ -65,10 +65,10 @@ __host__ __device__ inline void fill_head_params(int64_t c_int, int64_t dbound, 
     const uint64_t D = 2 * (uint64_t)c_eff;
     const uint64_t prod = (uint64_t)n_max * D;  // < 2^63
     int s = bitlen_u64(prod - 1) - 32;            // smallest s with prod <= 2^(32+s)
-    if (s < 0) s = 0;
+    if (s < 1) s = 1;  // s >= 1: the device applies >> s as umulhi(q, 2^(32-s))
     const uint64_t num = uint64_t(1) << (32 + s);
     const uint64_t M = (num + D - 1) / D;
-    if (M < (uint64_t(1) << 32)) {
+    if (s <= 31 && M < (uint64_t(1) << 32)) {
       hp->use32 = 1;
       hp->magic = (uint32_t)M;
       hp->shift = s;
@@ -88,29 +88,32 @@ __host__ __device__ inline void make_head_params(double c, int64_t d, int nlut, 
 }
 
 #ifdef __CUDACC__
-// Per-element index map (softmax.py:144-153), exact magic-number form (params.cuh).
-struct IdxMap {
-  int32_t lo;     // max(m - c_eff, INT32_MIN): a' = max(a, lo) clips delta to c_eff
-  uint32_t base;  // 2k*m + c_eff (mod 2^32)
-  uint32_t k2;    // 2k
-  uint32_t magic;
-  int shift;
-  __device__ __forceinline__ uint32_t idx(int32_t a) const {
-    const int32_t ac = max(a, lo);
-    const uint32_t n = base - k2 * (uint32_t)ac;  // n = 2k*delta' + c_eff in [c_eff, n_max]
-    return __umulhi(n, magic) >> shift;
-  }
-  __device__ __forceinline__ uint32_t idx_masked() const {
-    const uint32_t n = base - k2 * (uint32_t)lo;
-    return __umulhi(n, magic) >> shift;
-  }
-};
-
 // lo for a row max m.  If m - c_eff < INT32_MIN no int32 logit is clipped.
 __device__ __forceinline__ int32_t idx_lo(int32_t m, int64_t c_eff) {
   const int64_t lo = (int64_t)m - c_eff;
   return lo < (int64_t)INT32_MIN ? INT32_MIN : (int32_t)lo;
 }
+
+// Per-element index map (softmax.py:144-153), exact magic-number form (params.cuh).
+struct IdxMap {
+  int32_t lo;     // max(m - c_eff, INT32_MIN): a' = max(a, lo) clips delta to c_eff
+  uint32_t base;  // 2k*m + c_eff (mod 2^32)
+  uint32_t nk2;   // -2k (mod 2^32): n = base + nk2 * a' is one IMAD
+  uint32_t magic;
+  uint32_t mul2;  // 2^(32 - shift): q >> shift == umulhi(q, mul2) (keeps the shift on the FMA pipe)
+  __device__ __forceinline__ void init(int32_t m, const ia_head_params& hp, uint32_t k) {
+    nk2 = 0u - 2u * k;
+    magic = hp.magic;
+    mul2 = hp.use32 ? (1u << (32 - hp.shift)) : 0u;
+    lo = hp.use32 ? idx_lo(m, hp.c_eff) : 0;
+    base = (uint32_t)m * (2u * k) + (uint32_t)hp.c_eff;
+  }
+  __device__ __forceinline__ uint32_t idx(int32_t a) const {
+    const int32_t ac = max(a, lo);
+    const uint32_t n = base + nk2 * (uint32_t)ac;  // n = 2k*delta' + c_eff in [c_eff, n_max]
+    return __umulhi(__umulhi(n, magic), mul2);
+  }
+};
 
 __device__ __forceinline__ uint32_t idx_slow(int64_t m, int32_t a, int64_t c_eff, int64_t k) {
   int64_t dl = m - (int64_t)a;

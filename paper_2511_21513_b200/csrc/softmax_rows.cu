@@ -46,11 +46,7 @@ __global__ void __launch_bounds__(SR_THREADS)
       continue;
     }
     IdxMap im;
-    im.k2 = 2u * k;
-    im.magic = hp.magic;
-    im.shift = hp.shift;
-    im.lo = hp.use32 ? idx_lo(mx, hp.c_eff) : 0;
-    im.base = (uint32_t)mx * im.k2 + (uint32_t)hp.c_eff;
+    im.init(mx, hp, k);
     uint32_t s = 0;
     for (int64_t j = tid; j < cols; j += SR_THREADS) {  // softmax.py:144-155
       uint32_t idx;

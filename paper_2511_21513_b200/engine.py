@@ -27,13 +27,17 @@ MAX_SEQ_LEN = 65536
 FUSED_MAX_HEAD_DIM = 256
 
 
+_checked_devices = set()
+
+
 def require_device() -> torch.device:
     if not torch.cuda.is_available():
         raise RuntimeError("paper_2511_21513_b200 requires an sm_100 CUDA device; "
                            "there is no CPU fallback")
-    L = _lib.load()
     dev = torch.cuda.current_device()
-    _lib.check(L.ia_device_check(dev), "device check")
+    if dev not in _checked_devices:  # cudaGetDeviceProperties is slow: check once per device
+        _lib.check(_lib.load().ia_device_check(dev), "device check")
+        _checked_devices.add(dev)
     return torch.device("cuda", dev)
 
 
