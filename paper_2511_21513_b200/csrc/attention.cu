@@ -74,8 +74,9 @@ struct Cfg {
   static constexpr int OFF_K = Q_BYTES;
   static constexpr int OFF_V = OFF_K + NKST * K_BYTES;
   static constexpr int P_BYTES = BM * BN;  // u8 P^ tile, K-major SWIZZLE_128B (A of P.V)
+  static constexpr int NPB = DP <= 128 ? 2 : 1;  // P^ buffers per softmax warpgroup
   static constexpr int OFF_P = OFF_V + NVST * V_BYTES;
-  static constexpr int OFF_TAB = OFF_P + NWG * P_BYTES;
+  static constexpr int OFF_TAB = OFF_P + NWG * NPB * P_BYTES;
   static constexpr int KSTEPS = DP / 32;
   static constexpr int STAGE_PITCH = DP + 1;  // f32 epilogue staging row pitch (words, conflict-free)
   static_assert(OFF_TAB >= BM * STAGE_PITCH * 4, "epilogue staging must fit in Q/K/V stages");
@@ -88,7 +89,7 @@ template <int DP>
 constexpr size_t attn_smem_bytes(int nlut) {
   return 1024 /* alignment slack */ + (size_t)Cfg<DP>::OFF_TAB +
          (size_t)nlut * (wide_tab(nlut) ? 512 : 128) /* row tables */ +
-         2 * 3 * 512 /* row exchange */ + 256 /* barriers + tmem slot */;
+         2 * 3 * 512 /* row exchange */ + 512 /* barriers + tmem slot */;
 }
 
 // Masked-key bits for one 32-key chunk starting at j0 for query row i
@@ -133,11 +134,11 @@ __global__ void __launch_bounds__(Cfg<DP>::NTHREADS, 1)
   uint64_t* k_empty = k_full + C::NKST;
   uint64_t* v_full = k_empty + C::NKST;
   uint64_t* v_empty = v_full + NVST;
-  uint64_t* s_full = v_empty + NVST;  // [NWG] MMA -> softmax (QK^T landed in S[w])
-  uint64_t* s_free = s_full + NWG;    // [NWG] softmax -> MMA (S[w] fully read)
-  uint64_t* p_full = s_free + NWG;    // [NWG] softmax -> MMA (P^ tile w written to smem)
-  uint64_t* p_free = p_full + NWG;    // [NWG] MMA -> softmax (P.V finished reading P^ tile w)
-  uint64_t* o_full = p_free + NWG;    // MMA -> epilogue
+  uint64_t* s_full = v_empty + NVST;       // [NWG] QK issuer -> softmax (QK^T landed in S[w])
+  uint64_t* s_free = s_full + NWG;         // [NWG] softmax -> QK issuer (S[w] fully read)
+  uint64_t* p_full = s_free + NWG;         // [NWG*NPB] softmax -> P.V issuer (P^ tile in smem)
+  uint64_t* p_free = p_full + NWG * C::NPB;  // [NWG*NPB] P.V issuer -> softmax (tile consumed)
+  uint64_t* o_full = p_free + NWG * C::NPB;  // P.V issuer -> epilogue
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(o_full + 1);
 
   const int BH = p.B * p.H;
@@ -169,6 +170,8 @@ __global__ void __launch_bounds__(Cfg<DP>::NTHREADS, 1)
     for (int w = 0; w < NWG; ++w) {
       mbar_init(s_full + w, 1);
       mbar_init(s_free + w, 128);
+    }
+    for (int w = 0; w < NWG * C::NPB; ++w) {
       mbar_init(p_full + w, 128);
       mbar_init(p_free + w, 1);
     }
@@ -185,54 +188,51 @@ __global__ void __launch_bounds__(Cfg<DP>::NTHREADS, 1)
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
 
+  // Four single-thread roles: K producer (warp 0), QK^T issuer (warp 1), V^T
+  // producer (warp 2, after the TMEM allocation), P.V issuer (warp 3).  Keeping
+  // the two MMA streams in separate threads lets QK^T(n + NWG) start as soon as
+  // S[w] is read back, independent of P.V(n) progress.
   if (warp == 0) {
-    // ------------------------------------------------------------ TMA producer
+    // ------------------------------------------------------------ K producer (+ Q)
     if (lane == 0) {
       mbar_expect_tx(q_full, C::Q_BYTES);
       for (int s = 0; s < C::NSUB; ++s)
         tma_load_3d(smem + C::OFF_Q + s * C::SUB_BYTES, &tmq, q_full, s * C::SW, q0, bh);
-      // Load order == the MMA warp's consumption order (see below), so the K and
-      // V^T rings can never block each other.
-      int ks = 0, kph = 0, vs = 0, vph = 0;
-      auto load_k = [&](int n) {
+      int ks = 0, kph = 0;
+      const int nloads = (resident ? 1 : 3) * n_kt;
+      for (int t = 0; t < nloads; ++t) {
+        const int n = t % n_kt;
         mbar_wait(k_empty + ks, kph ^ 1);
         mbar_expect_tx(k_full + ks, C::K_BYTES);
         for (int s = 0; s < C::NSUB; ++s)
           tma_load_3d(smem + C::OFF_K + ks * C::K_BYTES + s * C::SUB_BYTES, &tmk, k_full + ks,
                       s * C::SW, n * BN, kvh);
         if (++ks == C::NKST) { ks = 0; kph ^= 1; }
-      };
-      auto load_v = [&](int n) {
+      }
+    }
+  } else if (warp == 2) {
+    // ------------------------------------------------------------ V^T producer
+    if (lane == 0) {
+      int vs = 0, vph = 0;
+      for (int n = 0; n < n_kt; ++n) {
         mbar_wait(v_empty + vs, vph ^ 1);
         mbar_expect_tx(v_full + vs, C::V_BYTES);
         tma_load_3d(smem + C::OFF_V + vs * C::V_BYTES, &tmv, v_full + vs, n * BN, 0, kvh);
         if (++vs == NVST) { vs = 0; vph ^= 1; }
-      };
-      if (resident) {
-        for (int n = 0; n < n_kt; ++n) load_k(n);
-        for (int n = 0; n < n_kt; ++n) load_v(n);
-      } else {
-        for (int pass = 0; pass < 2; ++pass)
-          for (int n = 0; n < n_kt; ++n) load_k(n);
-        for (int n = 0; n < NWG && n < n_kt; ++n) load_k(n);
-        for (int n = 0; n < n_kt; ++n) {
-          if (n + NWG < n_kt) load_k(n + NWG);
-          load_v(n);
-        }
       }
     }
   } else if (warp == 1) {
-    // ------------------------------------------------------------ MMA issuer
+    // ------------------------------------------------------------ QK^T issuer
     // Tile n of every pass lives in TMEM buffer / warpgroup w = n % NWG.
     if (lane == 0) {
-      constexpr uint32_t idq = idesc_i8(BM, BN, true, true);   // s8 x s8 -> s32
-      constexpr uint32_t idv = idesc_i8(BM, DP, false, true);  // u8 x s8 -> s32
+      constexpr uint32_t idq = idesc_i8(BM, BN, true, true);  // s8 x s8 -> s32
       const uint32_t sq = smem_u32(smem + C::OFF_Q);
       mbar_wait(q_full, 0);
-      int ks = 0, kph = 0, vs = 0, vph = 0;
-      uint32_t used = 0, c_s = 0, c_p = 0;  // per-buffer: occupied bit, s_free / p_full phases
-      auto issue_qk = [&](int n) {
-        const int w = n % NWG;
+      int ks = 0, kph = 0;
+      uint32_t used = 0, c_s = 0;  // per-buffer occupied bit / s_free phase
+      const int nmma = (resident ? 1 : 3) * n_kt;
+      for (int t = 0; t < nmma; ++t) {
+        const int w = (t % n_kt) % NWG;
         if ((used >> w) & 1u) { mbar_wait(s_free + w, (c_s >> w) & 1u); c_s ^= 1u << w; }
         used |= 1u << w;
         mbar_wait(k_full + ks, kph);
@@ -247,35 +247,28 @@ __global__ void __launch_bounds__(Cfg<DP>::NTHREADS, 1)
         tc_commit(k_empty + ks);
         tc_commit(s_full + w);
         if (++ks == C::NKST) { ks = 0; kph ^= 1; }
-      };
-      auto issue_pv = [&](int n) {
-        const int w = n % NWG;
-        mbar_wait(p_full + w, (c_p >> w) & 1u);
-        c_p ^= 1u << w;
+      }
+    }
+  } else if (warp == 3) {
+    // ------------------------------------------------------------ P.V issuer
+    if (lane == 0) {
+      constexpr uint32_t idv = idesc_i8(BM, DP, false, true);  // u8 x s8 -> s32
+      int vs = 0, vph = 0;
+      for (int n = 0; n < n_kt; ++n) {
+        const int w = n % NWG, tl = n / NWG;  // warpgroup and its local tile counter
+        const int pb = w * C::NPB + tl % C::NPB;
+        mbar_wait(p_full + pb, (uint32_t)(tl / C::NPB) & 1u);
         mbar_wait(v_full + vs, vph);
         tc_fence_after();
-        const uint32_t sp = smem_u32(smem + C::OFF_P + w * C::P_BYTES);
+        const uint32_t sp = smem_u32(smem + C::OFF_P + pb * C::P_BYTES);
         const uint32_t sv = smem_u32(smem + C::OFF_V + vs * C::V_BYTES);
 #pragma unroll
         for (int kk = 0; kk < BN / 32; ++kk)
           mma_i8_ss(tmem + C::O_COL, sdesc(sp + kk * 32, 1024, 2u), sdesc(sv + kk * 32, 1024, 2u),
                     idv, (n > 0 || kk > 0) ? 1u : 0u);
         tc_commit(v_empty + vs);
-        tc_commit(p_free + w);
+        tc_commit(p_free + pb);
         if (++vs == NVST) { vs = 0; vph ^= 1; }
-      };
-      if (!resident) {
-        for (int pass = 0; pass < 2; ++pass)
-          for (int n = 0; n < n_kt; ++n) issue_qk(n);
-        // pass 3: QK^T(n + NWG) only needs S[w] read back, so it runs ahead of P.V(n)
-        for (int n = 0; n < NWG && n < n_kt; ++n) issue_qk(n);
-        for (int n = 0; n < n_kt; ++n) {
-          if (n + NWG < n_kt) issue_qk(n + NWG);
-          issue_pv(n);
-        }
-      } else {
-        for (int n = 0; n < n_kt; ++n) issue_qk(n);
-        for (int n = 0; n < n_kt; ++n) issue_pv(n);
       }
       tc_commit(o_full);
     }
@@ -321,7 +314,9 @@ __global__ void __launch_bounds__(Cfg<DP>::NTHREADS, 1)
           }
         }
         if (!row_valid) continue;
-        const uint32_t ma = chunk_mask(p, i, j0, lim), mbb = chunk_mask(p, i, j0 + 32, lim);
+        const bool clean = (n * BN + BN - 1 <= lim) && !p.mask_bits;  // no masked key in tile
+        const uint32_t ma = clean ? 0u : chunk_mask(p, i, j0, lim);
+        const uint32_t mbb = clean ? 0u : chunk_mask(p, i, j0 + 32, lim);
         if ((ma | mbb) == 0) {
 #pragma unroll
           for (int e = 0; e < 32; e += 2)
@@ -365,11 +360,13 @@ __global__ void __launch_bounds__(Cfg<DP>::NTHREADS, 1)
         }
         if (!row_valid || dead) continue;
         const int j0 = n * BN + hb * 64;
-        const uint32_t ma = chunk_mask(p, i, j0, lim), mbb = chunk_mask(p, i, j0 + 32, lim);
+        const bool clean = (n * BN + BN - 1 <= lim) && !p.mask_bits;
+        const uint32_t ma = clean ? 0u : chunk_mask(p, i, j0, lim);
+        const uint32_t mbb = clean ? 0u : chunk_mask(p, i, j0 + 32, lim);
         if (fast && (ma | mbb) == 0) {
 #pragma unroll
           for (int e = 0; e < 32; ++e)
-            S += (uint32_t)lut8[im.idx((int32_t)va[e])] + (uint32_t)lut8[im.idx((int32_t)vb[e])];
+            S += (uint32_t)lut8[im.idx_s((int32_t)va[e])] + (uint32_t)lut8[im.idx_s((int32_t)vb[e])];
         } else {
 #pragma unroll
           for (int e = 0; e < 32; ++e) {
@@ -401,9 +398,9 @@ __global__ void __launch_bounds__(Cfg<DP>::NTHREADS, 1)
     const uint32_t tab_sh = wtab ? 9u : 7u;
     // this thread's row of its warpgroup's P^ tile (K-major, 128B swizzle: 16-byte
     // unit x of row r lives at unit x ^ (r % 8))
-    const uint32_t p_row = smem_u32(smem + C::OFF_P + wg * C::P_BYTES) + (uint32_t)row * 128;
+    const uint32_t p_rows = smem_u32(smem + C::OFF_P + wg * C::NPB * C::P_BYTES) + (uint32_t)row * 128;
     const uint32_t p_xor = (uint32_t)(row & 7);
-    uint32_t pf_ph = 0;
+    int tl = 0;  // this warpgroup's local pass-3 tile counter
 
     // ---- pass 3: P^ = rowtab[idx] -> smem -> P.V MMA (softmax.py:161-162)
     for (int n = wg; n < n_kt; n += NWG) {
@@ -412,8 +409,10 @@ __global__ void __launch_bounds__(Cfg<DP>::NTHREADS, 1)
         s_ph ^= 1u;
       }
       tc_fence_after();
-      mbar_wait(p_free + wg, pf_ph ^ 1u);  // previous P.V done with this P^ tile
-      pf_ph ^= 1u;
+      const int pbl = tl % C::NPB;
+      const uint32_t p_row = p_rows + (uint32_t)(pbl * C::P_BYTES);
+      // the P.V that last read this P^ buffer must be done (first use passes at once)
+      mbar_wait(p_free + wg * C::NPB + pbl, ((uint32_t)(tl / C::NPB) & 1u) ^ 1u);
 #pragma unroll 1
       for (int hb = 0; hb < BN / 64; ++hb) {
         uint32_t va[32], vb[32];
@@ -427,15 +426,17 @@ __global__ void __launch_bounds__(Cfg<DP>::NTHREADS, 1)
 #pragma unroll
         for (int q = 0; q < 16; ++q) pk[q] = 0u;
         if (row_valid && !dead) {
-          const uint32_t ma = chunk_mask(p, i, j0, lim), mbb = chunk_mask(p, i, j0 + 32, lim);
+          const bool clean = (n * BN + BN - 1 <= lim) && !p.mask_bits;
+          const uint32_t ma = clean ? 0u : chunk_mask(p, i, j0, lim);
+          const uint32_t mbb = clean ? 0u : chunk_mask(p, i, j0 + 32, lim);
           if (fast && wtab && (ma | mbb) == 0) {
 #pragma unroll
             for (int q = 0; q < 16; ++q) {
               const uint32_t* v4 = q < 8 ? &va[4 * q] : &vb[4 * (q - 8)];
-              const uint32_t p0 = lds_u32(tab_row + (im.idx((int32_t)v4[0]) << 9));
-              const uint32_t p1 = lds_u32(tab_row + (im.idx((int32_t)v4[1]) << 9));
-              const uint32_t p2 = lds_u32(tab_row + (im.idx((int32_t)v4[2]) << 9));
-              const uint32_t p3 = lds_u32(tab_row + (im.idx((int32_t)v4[3]) << 9));
+              const uint32_t p0 = lds_u32(tab_row + (im.idx_s((int32_t)v4[0]) << 9));
+              const uint32_t p1 = lds_u32(tab_row + (im.idx_s((int32_t)v4[1]) << 9));
+              const uint32_t p2 = lds_u32(tab_row + (im.idx_s((int32_t)v4[2]) << 9));
+              const uint32_t p3 = lds_u32(tab_row + (im.idx_s((int32_t)v4[3]) << 9));
               pk[q] = __byte_perm(__byte_perm(p0, p1, 0x0040), __byte_perm(p2, p3, 0x0040), 0x5410);
             }
           } else {
@@ -466,7 +467,8 @@ __global__ void __launch_bounds__(Cfg<DP>::NTHREADS, 1)
         }
       }
       fence_proxy_async_smem();
-      mbar_arrive(p_full + wg);
+      mbar_arrive(p_full + wg * C::NPB + pbl);
+      ++tl;
     }
 
     // ---- epilogue: out = f32(acc) * f32(s_v / scale) (pipeline.py:250-252)

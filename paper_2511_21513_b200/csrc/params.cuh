@@ -101,17 +101,26 @@ struct IdxMap {
   uint32_t nk2;   // -2k (mod 2^32): n = base + nk2 * a' is one IMAD
   uint32_t magic;
   uint32_t mul2;  // 2^(32 - shift): q >> shift == umulhi(q, mul2) (keeps the shift on the FMA pipe)
+  uint32_t shift;
   __device__ __forceinline__ void init(int32_t m, const ia_head_params& hp, uint32_t k) {
     nk2 = 0u - 2u * k;
     magic = hp.magic;
     mul2 = hp.use32 ? (1u << (32 - hp.shift)) : 0u;
+    shift = (uint32_t)hp.shift;
     lo = hp.use32 ? idx_lo(m, hp.c_eff) : 0;
     base = (uint32_t)m * (2u * k) + (uint32_t)hp.c_eff;
   }
+  // Two forms of the same exact map, to balance the FMA and ALU pipes:
+  // idx() does the final >> shift on the FMA pipe (IMAD.HI), idx_s() on the ALU pipe (SHF).
   __device__ __forceinline__ uint32_t idx(int32_t a) const {
     const int32_t ac = max(a, lo);
     const uint32_t n = base + nk2 * (uint32_t)ac;  // n = 2k*delta' + c_eff in [c_eff, n_max]
     return __umulhi(__umulhi(n, magic), mul2);
+  }
+  __device__ __forceinline__ uint32_t idx_s(int32_t a) const {
+    const int32_t ac = max(a, lo);
+    const uint32_t n = base + nk2 * (uint32_t)ac;
+    return __umulhi(n, magic) >> shift;
   }
 };
 
