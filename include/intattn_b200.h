@@ -133,9 +133,13 @@ typedef struct ia_attn_args {
   int32_t* dbg_logits; /* optional [B*H, L, L] int32 (debug/parity dump) */
   uint8_t* dbg_prob;   /* optional [B*H, L, L] u8 */
   int32_t* dbg_acc;    /* optional [B*H, L, d_pad] int32 */
+  long long* dbg_times; /* optional [grid, 16] int64 per-CTA phase clocks (zeroed; profiling) */
 } ia_attn_args;
 
 int ia_attn_fwd(const ia_attn_args* args, void* stream);
+/* IA_OK if the fused kernel supports (d_pad, 2^b LUT entries) within shared
+ * memory (d_pad 256 with b >= 6 does not); otherwise use the stage operators. */
+int ia_attn_supported(int64_t d_pad, int nlut);
 
 /* ------------------------------------------------------------------ stage operators
  * index_softmax (softmax.py:265-299 / :131-204): logits [rows, cols] int32,

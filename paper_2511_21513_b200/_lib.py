@@ -12,7 +12,7 @@ import subprocess
 import threading
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-SO_PATH = os.path.join(_HERE, "_lib", "libintattn_b200.so")
+SO_PATH = os.environ.get("IA_LIB") or os.path.join(_HERE, "_lib", "libintattn_b200.so")
 CSRC = os.path.join(_HERE, "csrc")
 
 IA_OK = 0
@@ -32,7 +32,7 @@ EXPORTS = (
     "ia_abi_version", "ia_status_string", "ia_last_error", "ia_device_check",
     "ia_quant_amax_rows", "ia_quant_amax_cols", "ia_quant_scales", "ia_quantize",
     "ia_dequantize", "ia_head_params_host", "ia_softmax_params_host", "ia_head_params_dev",
-    "ia_mask_pack", "ia_attn_fwd", "ia_index_softmax", "ia_gemm_i8",
+    "ia_mask_pack", "ia_attn_fwd", "ia_attn_supported", "ia_index_softmax", "ia_gemm_i8",
 )
 
 
@@ -53,7 +53,8 @@ class AttnArgs(ctypes.Structure):
                 ("l_pad", ctypes.c_int64), ("causal", ctypes.c_int32),
                 ("nlut", ctypes.c_int32), ("p_scale", ctypes.c_int32),
                 ("lut", ctypes.c_uint8 * 256), ("dbg_logits", ctypes.c_void_p),
-                ("dbg_prob", ctypes.c_void_p), ("dbg_acc", ctypes.c_void_p)]
+                ("dbg_prob", ctypes.c_void_p), ("dbg_acc", ctypes.c_void_p),
+                ("dbg_times", ctypes.c_void_p)]
 
 
 _lock = threading.Lock()
@@ -100,6 +101,7 @@ def load():
                                     i32, i32, P, P], i32),
             "ia_mask_pack": ([P, i64, P, P], i32),
             "ia_attn_fwd": ([ctypes.POINTER(AttnArgs), P], i32),
+            "ia_attn_supported": ([i64, i32], i32),
             "ia_index_softmax": ([P, i64, i64, ctypes.POINTER(HeadParams), P, i32, i32, P, P, P], i32),
             "ia_gemm_i8": ([P, i64, i32, P, i64, i64, i64, i64, P, i64, P], i32),
         }

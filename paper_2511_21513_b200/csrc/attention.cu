@@ -29,6 +29,8 @@
 // TMEM (512 columns): S[0] = cols [0,128), S[1] = [128,256), O = [256, 256+DP).
 #include <climits>
 #include <cstdint>
+#include <cstdlib>
+#include <cstring>
 
 #include "common.cuh"
 #include "params.cuh"
@@ -38,7 +40,6 @@ namespace ia {
 
 constexpr int BM = 128;  // query rows per tile (= TMEM lanes)
 constexpr int BN = 128;  // keys per tile
-constexpr int NVST = 2;  // V^T smem stages
 constexpr uint32_t TMEM_COLS = 512;
 
 struct AttnDev {
@@ -49,6 +50,7 @@ struct AttnDev {
   int32_t* dbg_logits;
   uint8_t* dbg_prob;
   int32_t* dbg_acc;
+  long long* dbg_times;  // optional per-CTA phase clocks (development instrumentation)
   int B, H, Hkv, L, d, mask_words;
   int causal, nlut, scale_x2, n_qt;
   uint8_t lut[256];
@@ -59,7 +61,7 @@ struct Cfg {
   // softmax warpgroups == TMEM S buffers (one 128-column buffer each); O sits after them.
   // Each warpgroup also owns one smem P^ tile.
   static constexpr int NWG = DP <= 128 ? 3 : 2;
-  static constexpr int NKST = DP <= 128 ? 3 : 2;  // K smem stages
+  static constexpr int NKST = DP <= 64 ? 6 : (DP <= 128 ? 3 : 2);  // K smem stages
   static constexpr int NTHREADS = 128 + 128 * NWG;
   static constexpr uint32_t O_COL = 128 * NWG;
   static constexpr int SW = DP >= 128 ? 128 : DP;  // swizzle span (bytes) of Q/K rows
@@ -72,6 +74,7 @@ struct Cfg {
   static constexpr int V_BYTES = DP * BN;  // V^T tile: DP rows x 128 keys, SWIZZLE_128B
   static constexpr int OFF_Q = 0;
   static constexpr int OFF_K = Q_BYTES;
+  static constexpr int NVST = 2;  // V^T smem stages
   static constexpr int OFF_V = OFF_K + NKST * K_BYTES;
   static constexpr int P_BYTES = BM * BN;  // u8 P^ tile, K-major SWIZZLE_128B (A of P.V)
   static constexpr int NPB = DP <= 128 ? 2 : 1;  // P^ buffers per softmax warpgroup
@@ -112,7 +115,30 @@ __device__ __forceinline__ uint32_t lds_u32(uint32_t addr) {
   return v;
 }
 
-template <int DP, bool DEBUG>
+// Phase / wait-time instrumentation (tools/phase_times.py).  Compiled in only
+// for the profiling build (make profile -> libintattn_b200_prof.so).
+#ifndef IA_PROFILE
+#define IA_PROFILE 0
+#endif
+__device__ __forceinline__ long long clk64() {
+#if IA_PROFILE
+  long long c;
+  asm volatile("mov.u64 %0, %%clock64;" : "=l"(c));
+  return c;
+#else
+  return 0;
+#endif
+}
+#define IA_TMARK(slot)                                                                      \
+  do {                                                                                      \
+    if (IA_PROFILE && p.dbg_times) p.dbg_times[(size_t)blockIdx.x * 16 + (slot)] = clk64(); \
+  } while (0)
+#define IA_TADD(slot, v)                                                                    \
+  do {                                                                                      \
+    if (IA_PROFILE && p.dbg_times) p.dbg_times[(size_t)blockIdx.x * 16 + (slot)] += (v);    \
+  } while (0)
+
+template <int DP, bool DEBUG, bool SKEL = false>
 __global__ void __launch_bounds__(Cfg<DP>::NTHREADS, 1)
     attn_fwd_kernel(const __grid_constant__ CUtensorMap tmq,
                     const __grid_constant__ CUtensorMap tmk,
@@ -133,8 +159,8 @@ __global__ void __launch_bounds__(Cfg<DP>::NTHREADS, 1)
   uint64_t* k_full = q_full + 1;
   uint64_t* k_empty = k_full + C::NKST;
   uint64_t* v_full = k_empty + C::NKST;
-  uint64_t* v_empty = v_full + NVST;
-  uint64_t* s_full = v_empty + NVST;       // [NWG] QK issuer -> softmax (QK^T landed in S[w])
+  uint64_t* v_empty = v_full + C::NVST;
+  uint64_t* s_full = v_empty + C::NVST;       // [NWG] QK issuer -> softmax (QK^T landed in S[w])
   uint64_t* s_free = s_full + NWG;         // [NWG] softmax -> QK issuer (S[w] fully read)
   uint64_t* p_full = s_free + NWG;         // [NWG*NPB] softmax -> P.V issuer (P^ tile in smem)
   uint64_t* p_free = p_full + NWG * C::NPB;  // [NWG*NPB] P.V issuer -> softmax (tile consumed)
@@ -156,6 +182,7 @@ __global__ void __launch_bounds__(Cfg<DP>::NTHREADS, 1)
     for (int t = threadIdx.x; t < rows * p.d; t += C::NTHREADS) o[t] = 0.0f;
     return;
   }
+  if (threadIdx.x == 0) IA_TMARK(6);
   const int key_end = p.causal ? min(q0 + BM, len) : len;
   const int n_kt = (key_end + BN - 1) / BN;
   const bool resident = n_kt <= NWG;  // every logit tile fits its own TMEM buffer
@@ -166,7 +193,7 @@ __global__ void __launch_bounds__(Cfg<DP>::NTHREADS, 1)
     prefetch_tmap(&tmv);
     mbar_init(q_full, 1);
     for (int s = 0; s < C::NKST; ++s) { mbar_init(k_full + s, 1); mbar_init(k_empty + s, 1); }
-    for (int s = 0; s < NVST; ++s) { mbar_init(v_full + s, 1); mbar_init(v_empty + s, 1); }
+    for (int s = 0; s < C::NVST; ++s) { mbar_init(v_full + s, 1); mbar_init(v_empty + s, 1); }
     for (int w = 0; w < NWG; ++w) {
       mbar_init(s_full + w, 1);
       mbar_init(s_free + w, 128);
@@ -218,7 +245,7 @@ __global__ void __launch_bounds__(Cfg<DP>::NTHREADS, 1)
         mbar_wait(v_empty + vs, vph ^ 1);
         mbar_expect_tx(v_full + vs, C::V_BYTES);
         tma_load_3d(smem + C::OFF_V + vs * C::V_BYTES, &tmv, v_full + vs, n * BN, 0, kvh);
-        if (++vs == NVST) { vs = 0; vph ^= 1; }
+        if (++vs == C::NVST) { vs = 0; vph ^= 1; }
       }
     }
   } else if (warp == 1) {
@@ -233,9 +260,14 @@ __global__ void __launch_bounds__(Cfg<DP>::NTHREADS, 1)
       const int nmma = (resident ? 1 : 3) * n_kt;
       for (int t = 0; t < nmma; ++t) {
         const int w = (t % n_kt) % NWG;
+        long long t0 = clk64();
         if ((used >> w) & 1u) { mbar_wait(s_free + w, (c_s >> w) & 1u); c_s ^= 1u << w; }
         used |= 1u << w;
+        long long t1 = clk64();
         mbar_wait(k_full + ks, kph);
+        long long t2 = clk64();
+        IA_TADD(8, t1 - t0);
+        IA_TADD(9, t2 - t1);
         tc_fence_after();
         const uint32_t sk = smem_u32(smem + C::OFF_K + ks * C::K_BYTES);
 #pragma unroll
@@ -257,8 +289,13 @@ __global__ void __launch_bounds__(Cfg<DP>::NTHREADS, 1)
       for (int n = 0; n < n_kt; ++n) {
         const int w = n % NWG, tl = n / NWG;  // warpgroup and its local tile counter
         const int pb = w * C::NPB + tl % C::NPB;
+        long long t0 = clk64();
         mbar_wait(p_full + pb, (uint32_t)(tl / C::NPB) & 1u);
+        long long t1 = clk64();
         mbar_wait(v_full + vs, vph);
+        long long t2 = clk64();
+        IA_TADD(11, t1 - t0);
+        IA_TADD(12, t2 - t1);
         tc_fence_after();
         const uint32_t sp = smem_u32(smem + C::OFF_P + pb * C::P_BYTES);
         const uint32_t sv = smem_u32(smem + C::OFF_V + vs * C::V_BYTES);
@@ -268,7 +305,7 @@ __global__ void __launch_bounds__(Cfg<DP>::NTHREADS, 1)
                     idv, (n > 0 || kk > 0) ? 1u : 0u);
         tc_commit(v_empty + vs);
         tc_commit(p_free + pb);
-        if (++vs == NVST) { vs = 0; vph ^= 1; }
+        if (++vs == C::NVST) { vs = 0; vph ^= 1; }
       }
       tc_commit(o_full);
     }
@@ -290,12 +327,17 @@ __global__ void __launch_bounds__(Cfg<DP>::NTHREADS, 1)
     // Each tile is read from TMEM in two 64-column batches (two x32 loads in
     // flight per wait); S[w] is handed back to the MMA warp right after the last
     // load of the tile, in every pass.
+    const bool tm = (threadIdx.x == 128);
+    if (tm) IA_TMARK(0);
     // ---- pass 1: row max over unmasked keys (softmax.py:139-143, :174-179)
     int32_t mx = INT_MIN;
     for (int n = wg; n < n_kt; n += NWG) {
+      long long tw0 = clk64();
       mbar_wait(s_full + wg, s_ph);
       s_ph ^= 1u;
+      if (tm) IA_TADD(15, clk64() - tw0);
       tc_fence_after();
+      const bool clean = (n * BN + BN - 1 <= lim) && !p.mask_bits;  // no masked key in tile
 #pragma unroll 1
       for (int hb = 0; hb < BN / 64; ++hb) {
         uint32_t va[32], vb[32];
@@ -314,9 +356,11 @@ __global__ void __launch_bounds__(Cfg<DP>::NTHREADS, 1)
           }
         }
         if (!row_valid) continue;
-        const bool clean = (n * BN + BN - 1 <= lim) && !p.mask_bits;  // no masked key in tile
-        const uint32_t ma = clean ? 0u : chunk_mask(p, i, j0, lim);
-        const uint32_t mbb = clean ? 0u : chunk_mask(p, i, j0 + 32, lim);
+        uint32_t ma = 0u, mbb = 0u;
+        if (__builtin_expect(!clean, 0)) {
+          ma = chunk_mask(p, i, j0, lim);
+          mbb = chunk_mask(p, i, j0 + 32, lim);
+        }
         if ((ma | mbb) == 0) {
 #pragma unroll
           for (int e = 0; e < 32; e += 2)
@@ -331,6 +375,7 @@ __global__ void __launch_bounds__(Cfg<DP>::NTHREADS, 1)
         }
       }
     }
+    if (tm) IA_TMARK(1);
     xmax[wg * 128 + row] = mx;
     named_bar_sync(1, NWT);
     int32_t m = xmax[row];
@@ -346,10 +391,13 @@ __global__ void __launch_bounds__(Cfg<DP>::NTHREADS, 1)
     uint32_t S = 0;
     for (int n = wg; n < n_kt; n += NWG) {
       if (!resident) {
+        long long tw0 = clk64();
         mbar_wait(s_full + wg, s_ph);
         s_ph ^= 1u;
+        if (tm) IA_TADD(14, clk64() - tw0);
       }
       tc_fence_after();
+      const bool clean = (n * BN + BN - 1 <= lim) && !p.mask_bits;
 #pragma unroll 1
       for (int hb = 0; hb < BN / 64; ++hb) {
         uint32_t va[32], vb[32];
@@ -358,11 +406,13 @@ __global__ void __launch_bounds__(Cfg<DP>::NTHREADS, 1)
           tc_fence_before();
           mbar_arrive(s_free + wg);
         }
-        if (!row_valid || dead) continue;
+        if (!row_valid || dead || SKEL) continue;
         const int j0 = n * BN + hb * 64;
-        const bool clean = (n * BN + BN - 1 <= lim) && !p.mask_bits;
-        const uint32_t ma = clean ? 0u : chunk_mask(p, i, j0, lim);
-        const uint32_t mbb = clean ? 0u : chunk_mask(p, i, j0 + 32, lim);
+        uint32_t ma = 0u, mbb = 0u;
+        if (__builtin_expect(!clean, 0)) {
+          ma = chunk_mask(p, i, j0, lim);
+          mbb = chunk_mask(p, i, j0 + 32, lim);
+        }
         if (fast && (ma | mbb) == 0) {
 #pragma unroll
           for (int e = 0; e < 32; ++e)
@@ -378,6 +428,7 @@ __global__ void __launch_bounds__(Cfg<DP>::NTHREADS, 1)
         }
       }
     }
+    if (tm) IA_TMARK(2);
     xsum[wg * 128 + row] = S;
     named_bar_sync(1, NWT);
     S = xsum[row];
@@ -405,14 +456,19 @@ __global__ void __launch_bounds__(Cfg<DP>::NTHREADS, 1)
     // ---- pass 3: P^ = rowtab[idx] -> smem -> P.V MMA (softmax.py:161-162)
     for (int n = wg; n < n_kt; n += NWG) {
       if (!resident) {
+        long long tw0 = clk64();
         mbar_wait(s_full + wg, s_ph);
         s_ph ^= 1u;
+        if (tm) IA_TADD(14, clk64() - tw0);
       }
       tc_fence_after();
+      const bool clean = (n * BN + BN - 1 <= lim) && !p.mask_bits;
       const int pbl = tl % C::NPB;
       const uint32_t p_row = p_rows + (uint32_t)(pbl * C::P_BYTES);
       // the P.V that last read this P^ buffer must be done (first use passes at once)
+      long long tq0 = clk64();
       mbar_wait(p_free + wg * C::NPB + pbl, ((uint32_t)(tl / C::NPB) & 1u) ^ 1u);
+      if (tm) IA_TADD(13, clk64() - tq0);
 #pragma unroll 1
       for (int hb = 0; hb < BN / 64; ++hb) {
         uint32_t va[32], vb[32];
@@ -425,10 +481,12 @@ __global__ void __launch_bounds__(Cfg<DP>::NTHREADS, 1)
         uint32_t pk[16];
 #pragma unroll
         for (int q = 0; q < 16; ++q) pk[q] = 0u;
-        if (row_valid && !dead) {
-          const bool clean = (n * BN + BN - 1 <= lim) && !p.mask_bits;
-          const uint32_t ma = clean ? 0u : chunk_mask(p, i, j0, lim);
-          const uint32_t mbb = clean ? 0u : chunk_mask(p, i, j0 + 32, lim);
+        if (row_valid && !dead && !SKEL) {
+          uint32_t ma = 0u, mbb = 0u;
+          if (__builtin_expect(!clean, 0)) {
+            ma = chunk_mask(p, i, j0, lim);
+            mbb = chunk_mask(p, i, j0 + 32, lim);
+          }
           if (fast && wtab && (ma | mbb) == 0) {
 #pragma unroll
             for (int q = 0; q < 16; ++q) {
@@ -474,7 +532,9 @@ __global__ void __launch_bounds__(Cfg<DP>::NTHREADS, 1)
     // ---- epilogue: out = f32(acc) * f32(s_v / scale) (pipeline.py:250-252)
     // TMEM -> registers -> smem staging (all TMA/MMA traffic has drained once
     // o_full fires) -> coalesced row-contiguous global stores.
+    if (tm) IA_TMARK(3);
     mbar_wait(o_full, 0);
+    if (tm) IA_TMARK(4);
     tc_fence_after();
     float* stage = reinterpret_cast<float*>(smem);
     const float osc = hp.out_scale;
@@ -512,6 +572,7 @@ __global__ void __launch_bounds__(Cfg<DP>::NTHREADS, 1)
 
   tc_fence_before();
   __syncthreads();
+  if (threadIdx.x == 0) { IA_TMARK(5); if (IA_PROFILE && p.dbg_times) p.dbg_times[(size_t)blockIdx.x * 16 + 10] = n_kt; }
   if (warp == 2) {
     tc_fence_after();
     tmem_dealloc(tmem, TMEM_COLS);
@@ -522,9 +583,17 @@ __global__ void __launch_bounds__(Cfg<DP>::NTHREADS, 1)
 int make_tmap_3d(CUtensorMap* m, const void* base, uint64_t d0, uint64_t d1, uint64_t d2,
                  uint64_t stride1, uint64_t stride2, uint32_t b0, uint32_t b1, int swizzle_bytes);
 
-template <int DP, bool DEBUG>
+template <int DP>
+bool attn_supported(int nlut) {
+  return attn_smem_bytes<DP>(nlut) + 256 <= 227 * 1024;
+}
+
+template <int DP, bool DEBUG, bool SKEL = false>
 static int launch_attn(const ia_attn_args* a, cudaStream_t st) {
   using C = Cfg<DP>;
+  if (!attn_supported<DP>(a->nlut))
+    return fail(IA_ERR_HEAD_DIM, "fused path: d_pad %d with %d LUT entries exceeds shared memory",
+                DP, a->nlut);
   CUtensorMap tq, tk, tv;
   const uint64_t BH = a->B * a->H, BHkv = a->B * a->Hkv;
   int r;
@@ -545,6 +614,7 @@ static int launch_attn(const ia_attn_args* a, cudaStream_t st) {
   dv.dbg_logits = a->dbg_logits;
   dv.dbg_prob = a->dbg_prob;
   dv.dbg_acc = a->dbg_acc;
+  dv.dbg_times = a->dbg_times;
   dv.B = (int)a->B;
   dv.H = (int)a->H;
   dv.Hkv = (int)a->Hkv;
@@ -558,7 +628,7 @@ static int launch_attn(const ia_attn_args* a, cudaStream_t st) {
   for (int t = 0; t < 256; ++t) dv.lut[t] = t < a->nlut ? a->lut[t] : 0;
   size_t smem = attn_smem_bytes<DP>(a->nlut);
   if (smem < 120 * 1024) smem = 120 * 1024;  // one CTA per SM (it owns all 512 TMEM columns)
-  auto kern = attn_fwd_kernel<DP, DEBUG>;
+  auto kern = attn_fwd_kernel<DP, DEBUG, SKEL>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return fail(IA_ERR_CUDA, "smem attribute: %s", cudaGetErrorString(e));
   const uint64_t grid = (uint64_t)dv.n_qt * BH;
@@ -570,6 +640,16 @@ static int launch_attn(const ia_attn_args* a, cudaStream_t st) {
 }  // namespace ia
 
 using namespace ia;
+
+extern "C" int ia_attn_supported(int64_t d_pad, int nlut) {
+  switch (d_pad) {
+    case 32: return attn_supported<32>(nlut) ? IA_OK : IA_ERR_HEAD_DIM;
+    case 64: return attn_supported<64>(nlut) ? IA_OK : IA_ERR_HEAD_DIM;
+    case 128: return attn_supported<128>(nlut) ? IA_OK : IA_ERR_HEAD_DIM;
+    case 256: return attn_supported<256>(nlut) ? IA_OK : IA_ERR_HEAD_DIM;
+    default: return IA_ERR_HEAD_DIM;
+  }
+}
 
 extern "C" int ia_attn_fwd(const ia_attn_args* a, void* stream) {
   if (!a || !a->q || !a->k || !a->vt || !a->out || !a->params)
@@ -595,7 +675,12 @@ extern "C" int ia_attn_fwd(const ia_attn_args* a, void* stream) {
   switch (a->d_pad) {
     case 32: return dbg ? launch_attn<32, true>(a, st) : launch_attn<32, false>(a, st);
     case 64: return dbg ? launch_attn<64, true>(a, st) : launch_attn<64, false>(a, st);
-    case 128: return dbg ? launch_attn<128, true>(a, st) : launch_attn<128, false>(a, st);
+    case 128:
+      // IA_EXPERIMENT=skeleton: timing-only variant (softmax reads TMEM, skips the
+      // integer work; output is NOT IndexSoftmax).  Never used by the library API.
+      if (!dbg && getenv("IA_EXPERIMENT") && !strcmp(getenv("IA_EXPERIMENT"), "skeleton"))
+        return launch_attn<128, false, true>(a, st);
+      return dbg ? launch_attn<128, true>(a, st) : launch_attn<128, false>(a, st);
     default: return dbg ? launch_attn<256, true>(a, st) : launch_attn<256, false>(a, st);
   }
 }

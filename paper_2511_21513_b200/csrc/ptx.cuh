@@ -29,15 +29,28 @@ __device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
 // try_wait with a suspend-time hint: the waiting warp sleeps in hardware until
 // the phase completes (or ~1 ms passes) instead of spinning, so idle waits do
 // not steal issue slots from the softmax warps sharing its SM sub-partition.
+#ifndef IA_WAIT_HINT_NS
+#define IA_WAIT_HINT_NS 1000000
+#endif
 __device__ __forceinline__ uint32_t mbar_try_wait(uint32_t bar, uint32_t parity) {
   uint32_t ok;
+#if IA_WAIT_HINT_NS > 0
   asm volatile(
       "{\n\t.reg .pred p;\n\t"
       "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n\t"
       "selp.u32 %0, 1, 0, p;\n\t}"
       : "=r"(ok)
-      : "r"(bar), "r"(parity), "r"(1000000u)
+      : "r"(bar), "r"(parity), "r"((uint32_t)IA_WAIT_HINT_NS)
       : "memory");
+#else
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+      "selp.u32 %0, 1, 0, p;\n\t}"
+      : "=r"(ok)
+      : "r"(bar), "r"(parity)
+      : "memory");
+#endif
   return ok;
 }
 
@@ -48,7 +61,28 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   const uint32_t a = smem_u32(bar);
   uint32_t spins = 0;
   while (!mbar_try_wait(a, parity)) {
-    if (++spins > 8000u) __trap();
+    if (++spins > (IA_WAIT_HINT_NS > 0 ? 8000u : 400000000u)) __trap();
+  }
+}
+
+// Busy-poll variant for the single-thread producer / MMA-issuer roles, where the
+// ~220-cycle sleep wake-up would sit on the pipeline's critical path.
+__device__ __forceinline__ uint32_t mbar_poll(uint32_t bar, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+      "selp.u32 %0, 1, 0, p;\n\t}"
+      : "=r"(ok)
+      : "r"(bar), "r"(parity)
+      : "memory");
+  return ok;
+}
+__device__ __forceinline__ void mbar_wait_spin(uint64_t* bar, uint32_t parity) {
+  const uint32_t a = smem_u32(bar);
+  uint32_t spins = 0;
+  while (!mbar_poll(a, parity)) {
+    if (++spins > 400000000u) __trap();
   }
 }
 

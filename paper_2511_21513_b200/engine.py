@@ -182,7 +182,7 @@ def prepare(q, k, v, *, seq_lens=None, scale_granularity="head", b=5, c=6.6, p_s
 
 
 def attn_fused(prep: Prepared, shape, out, *, causal=False, seq_lens=None, mask_bits=None,
-               lut=None, p_scale=255, debug=None):
+               lut=None, p_scale=255, debug=None, times=None):
     B, H, Hkv, Lq, d = shape
     a = _lib.AttnArgs()
     a.q, a.k, a.vt = prep.qhat.data_ptr(), prep.khat.data_ptr(), prep.vt.data_ptr()
@@ -200,6 +200,8 @@ def attn_fused(prep: Prepared, shape, out, *, causal=False, seq_lens=None, mask_
         a.dbg_logits = debug["logits"].data_ptr()
         a.dbg_prob = debug["prob"].data_ptr()
         a.dbg_acc = debug["acc"].data_ptr()
+    if times is not None:
+        a.dbg_times = times.data_ptr()
     _lib.check(_lib.load().ia_attn_fwd(ctypes.byref(a), _stream()), "attention")
 
 
@@ -233,6 +235,8 @@ def attention(q, k, v, *, causal=False, seq_lens=None, mask=None, scale_granular
     if timer is not None:
         timer.mark("start")
     d_pad = pad_head_dim(d)
+    if d_pad is not None and _lib.load().ia_attn_supported(d_pad, len(lut)) != _lib.IA_OK:
+        d_pad = None  # e.g. d_pad 256 with a 2^6+ entry LUT: shared memory too small
     if d_pad is None:
         res = _attention_unfused(q, k, v, causal=causal, seq_lens=seq_lens, mask=mask,
                                  scale_granularity=scale_granularity, b=b, c=c,
