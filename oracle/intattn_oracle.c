@@ -167,7 +167,8 @@ void ia_or_index_softmax(const int32_t* logits, int64_t rows, int64_t cols,
  * (pipeline.py:202-256) applied per unit, as SURVEY.md §3.5/§8d composes it:
  *   q [B,H,L,d], k/v [B,Hkv,L,d] f32; query head h uses KV head h/(H/Hkv).
  *   scale_mode 0: per (b,head) slab over its valid rows; 1: one global scale
- *   per tensor (over valid rows).  seq_lens (nullable) [B]: rows >= len are
+ *   per tensor (over valid rows); 2: given global scales (qs_out[0],
+ *   ks_out[0], vs_out[0] are inputs -- the sharded launcher's all-reduced amax).  seq_lens (nullable) [B]: rows >= len are
  *   padding (excluded from amax, masked as keys, zero output as queries).
  *   causal: key j > query i masked.  mask (nullable) [L,L] u8 shared by all
  *   units (True = excluded).  row_stride > 1 computes only rows i with
@@ -218,7 +219,10 @@ int ia_or_attention_batched(const float* q, const float* k, const float* v,
       bad |= nf;
     }
     if (bad) status = OR_ERR_NONFINITE;
-    if (scale_mode == 1) {
+    if (scale_mode == 2) {
+      const float* given[3] = {qs_out, ks_out, vs_out};
+      for (int64_t u = 0; u < B * nh; ++u) scs[t][u] = given[t][0];
+    } else if (scale_mode == 1) {
       float g = 0.0f;
       for (int64_t u = 0; u < B * nh; ++u) g = amax[u] > g ? amax[u] : g;
       for (int64_t u = 0; u < B * nh; ++u) scs[t][u] = ia_or_scale(g);
@@ -235,9 +239,11 @@ int ia_or_attention_batched(const float* q, const float* k, const float* v,
     }
   }
   if (status != OR_OK) goto done;
-  if (qs_out) memcpy(qs_out, sq, sizeof(float) * B * H);
-  if (ks_out) memcpy(ks_out, sk, sizeof(float) * B * Hkv);
-  if (vs_out) memcpy(vs_out, sv, sizeof(float) * B * Hkv);
+  if (scale_mode != 2) {
+    if (qs_out) memcpy(qs_out, sq, sizeof(float) * B * H);
+    if (ks_out) memcpy(ks_out, sk, sizeof(float) * B * Hkv);
+    if (vs_out) memcpy(vs_out, sv, sizeof(float) * B * Hkv);
+  }
 
   {
     int64_t* cint = (int64_t*)malloc(sizeof(int64_t) * B * H);

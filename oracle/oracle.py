@@ -162,7 +162,7 @@ def int_attention(q, k, v, b=5, c=6.6, mask=None, p_scale=P_UINT8X255):
 
 def attention_batched(q, k, v, *, causal=False, seq_lens=None, mask=None,
                       scale_granularity="head", b=5, c=6.6, p_scale=P_UINT8X255,
-                      row_stride=1, threads=0, lut=None):
+                      row_stride=1, threads=0, lut=None, scales=None):
     """Batched oracle (see ia_or_attention_batched).  Returns (out, info)."""
     q = np.ascontiguousarray(q, np.float32)
     k = np.ascontiguousarray(k, np.float32)
@@ -178,6 +178,9 @@ def attention_batched(q, k, v, *, causal=False, seq_lens=None, mask=None,
     vs = np.empty(B * Hkv, np.float32)
     ci = np.empty(B * H, np.int64)
     mode = {"head": 0, "tensor": 1}[scale_granularity]
+    if scales is not None:  # given global scales (sharded launcher)
+        mode = 2
+        qs[0], ks[0], vs[0] = (np.float32(s) for s in scales)
     st = lib().ia_or_attention_batched(
         _p(q), _p(k), _p(v), B, H, Hkv, L, d, _p(sl), int(bool(causal)), _p(m8),
         mode, float(c), _p(lut), lut.size, int(p_scale), int(row_stride),

@@ -142,15 +142,20 @@ HEAD_PARAMS_BYTES = ctypes.sizeof(_lib.HeadParams)
 
 
 def prepare(q, k, v, *, seq_lens=None, scale_granularity="head", b=5, c=6.6, p_scale=255,
-            d_pad=None) -> Prepared:
-    """Quantise Q/K/V on device and compute per-(b, h) parameters."""
+            d_pad=None, scales=None) -> Prepared:
+    """Quantise Q/K/V on device and compute per-(b, h) parameters.
+
+    ``scales`` (optional): precomputed global (q, k, v) f32 scales as 1-element
+    device tensors -- the sharded launcher's all-reduced amax; implies
+    ``scale_granularity="tensor"`` and skips the amax kernels.
+    """
     B, H, Lq, d = q.shape
     Hkv = k.shape[1]
     dev = q.device
     if d_pad is None:
         d_pad = pad_head_dim(d)
     l_pad = _round_up(Lq, 16)
-    per_head = scale_granularity == "head"
+    per_head = scale_granularity == "head" and scales is None
     nq = B * H if per_head else 1
     nkv = B * Hkv if per_head else 1
     ws = Workspace(nq + 2 * nkv, dev)
@@ -158,13 +163,17 @@ def prepare(q, k, v, *, seq_lens=None, scale_granularity="head", b=5, c=6.6, p_s
     ak, sk = ws.take(nkv)
     av, sv = ws.take(nkv)
     sl = seq_lens
-    amax_rows(q, B * H, Lq, d, aq, ws.err, seq_lens=sl, valid_div=H,
-              slot_div=1 if per_head else B * H)
-    amax_rows(k, B * Hkv, Lq, d, ak, ws.err, seq_lens=sl, valid_div=Hkv,
-              slot_div=1 if per_head else B * Hkv)
-    amax_rows(v, B * Hkv, Lq, d, av, ws.err, seq_lens=sl, valid_div=Hkv,
-              slot_div=1 if per_head else B * Hkv)
-    scales_from_amax(ws.amax, ws.scales)
+    if scales is None:
+        amax_rows(q, B * H, Lq, d, aq, ws.err, seq_lens=sl, valid_div=H,
+                  slot_div=1 if per_head else B * H)
+        amax_rows(k, B * Hkv, Lq, d, ak, ws.err, seq_lens=sl, valid_div=Hkv,
+                  slot_div=1 if per_head else B * Hkv)
+        amax_rows(v, B * Hkv, Lq, d, av, ws.err, seq_lens=sl, valid_div=Hkv,
+                  slot_div=1 if per_head else B * Hkv)
+        scales_from_amax(ws.amax, ws.scales)
+    else:
+        for dst, src in zip((sq, sk, sv), scales):
+            dst.copy_(src.reshape(1))
     qhat = torch.empty((B * H, Lq, d_pad), dtype=torch.int8, device=dev)
     khat = torch.empty((B * Hkv, Lq, d_pad), dtype=torch.int8, device=dev)
     vt = torch.empty((B * Hkv, d_pad, l_pad), dtype=torch.int8, device=dev)
@@ -217,7 +226,7 @@ def lut_bytes(b: int, c: float) -> np.ndarray:
 
 def attention(q, k, v, *, causal=False, seq_lens=None, mask=None, scale_granularity="head",
               b=5, c=6.6, p_scale=255, lut=None, out=None, debug=False, check_finite=True,
-              timer=None):
+              timer=None, scales=None):
     """Batched fused IntAttention on the current CUDA device.
 
     q [B, H, L, d], k/v [B, Hkv, L, d]: f32 CUDA tensors (contiguous).
@@ -238,6 +247,8 @@ def attention(q, k, v, *, causal=False, seq_lens=None, mask=None, scale_granular
     if d_pad is not None and _lib.load().ia_attn_supported(d_pad, len(lut)) != _lib.IA_OK:
         d_pad = None  # e.g. d_pad 256 with a 2^6+ entry LUT: shared memory too small
     if d_pad is None:
+        if scales is not None:
+            raise ValueError("precomputed scales need the fused path (head dim <= 256)")
         res = _attention_unfused(q, k, v, causal=causal, seq_lens=seq_lens, mask=mask,
                                  scale_granularity=scale_granularity, b=b, c=c,
                                  p_scale=p_scale, lut=lut, out=out, check_finite=check_finite)
@@ -246,7 +257,7 @@ def attention(q, k, v, *, causal=False, seq_lens=None, mask=None, scale_granular
             timer.mark("attention")
         return (res, {}) if debug else res
     prep = prepare(q, k, v, seq_lens=seq_lens, scale_granularity=scale_granularity, b=b, c=c,
-                   p_scale=p_scale, d_pad=d_pad)
+                   p_scale=p_scale, d_pad=d_pad, scales=scales)
     mbits = pack_mask(mask) if mask is not None else None
     if timer is not None:
         timer.mark("quantized")

@@ -1,0 +1,116 @@
+"""C-ABI checks that need no GPU: the library loads, exports every symbol the
+header declares, and its host-side parameter math (c_int, the exact
+magic-number index map) is right.  The product path must refuse to run
+without a device (no CPU fallback)."""
+import ctypes
+import os
+import re
+
+import numpy as np
+import pytest
+import torch
+
+from golden_io import f32, stage_cases
+from oracle import oracle as O
+from paper_2511_21513_b200 import _lib
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+HEADER = os.path.join(ROOT, "include", "intattn_b200.h")
+
+
+def header_functions():
+    txt = open(HEADER).read()
+    return sorted(set(re.findall(r"^\s*(?:int|const char\*)\s+(ia_\w+)\s*\(", txt, re.M)))
+
+
+def test_library_loads_and_exports_every_declared_symbol():
+    L = _lib.load()
+    declared = header_functions()
+    assert len(declared) >= 16
+    for name in declared:
+        assert hasattr(L, name), f"{name} declared in include/intattn_b200.h but not exported"
+    assert sorted(_lib.EXPORTS) == declared
+    assert L.ia_abi_version() == 1
+
+
+def test_status_strings():
+    L = _lib.load()
+    for code in range(8):
+        assert L.ia_status_string(code)
+    assert L.ia_status_string(4).decode() == "input contains non-finite elements"
+
+
+def test_no_device_raises():
+    if torch.cuda.is_available():
+        pytest.skip("a device is present")
+    L = _lib.load()
+    assert L.ia_device_check(0) == _lib.IA_ERR_NO_DEVICE
+    import paper_2511_21513_b200 as ia
+    x = np.ones((4, 8), np.float32)
+    with pytest.raises(RuntimeError):
+        ia.int_attention(x, x, x)
+    with pytest.raises(RuntimeError):
+        ia.quantize_symmetric(x)
+
+
+@pytest.mark.parametrize("idx", range(0, len(stage_cases()), 7))
+def test_c_int_matches_reference(idx):
+    row = stage_cases()[idx]
+    case = row["case"]
+    d = case["d"]
+    p = case["p"]
+    hp = _lib.head_params_host(case["c"], d, 1 << case["b"], p, f32(row["sq"]), f32(row["sk"]),
+                               f32(row["sv"]))
+    assert hp.c_int == row["c_int"]
+    assert hp.out_scale == np.float32(float(f32(row["sv"])) / p)
+
+
+def _check_map(hp, k, deltas):
+    """Device index map (softmax.py:144-153 via params.cuh) vs exact integer division."""
+    c_eff = hp.c_eff
+    dp = np.minimum(deltas.astype(np.int64), c_eff)
+    n = (2 * k * dp + c_eff).astype(np.uint64)
+    want = n // np.uint64(2 * c_eff)
+    if hp.use32:
+        assert int(n.max()) < (1 << 31)
+        q = (n * np.uint64(hp.magic)) >> np.uint64(32)
+        got_shf = q >> np.uint64(hp.shift)
+        got_mul = (q * np.uint64(1 << (32 - hp.shift))) >> np.uint64(32)
+        assert np.array_equal(got_shf, want)
+        assert np.array_equal(got_mul, want)
+
+
+@pytest.mark.parametrize("b", [2, 5, 8])
+@pytest.mark.parametrize("d", [1, 64, 128, 256])
+def test_magic_index_map_exhaustive(b, d):
+    """Exhaustive over every reachable clipped distance for a spread of c_int."""
+    k = (1 << b) - 1
+    rng = np.random.default_rng(b * 1000 + d)
+    c_values = [1, 2, 3, 50, 614, 716, 37335, 45302, 63190, 1 << 20, 1 << 40, 1 << 52]
+    c_values += [int(x) for x in rng.integers(1, 200000, size=6)]
+    dbound = 2 * d * 127 * 127
+    for ci in c_values:
+        hp = _lib.softmax_params_host(ci, dbound, 1 << b)
+        c_eff = hp.c_eff
+        assert c_eff == min(ci, 2 * k * dbound + 1)
+        top = min(c_eff, dbound)
+        if top <= 3_000_000:
+            deltas = np.arange(0, top + 1, dtype=np.int64)
+        else:
+            deltas = np.unique(np.concatenate([rng.integers(0, top + 1, 2_000_000),
+                                               np.arange(0, 1000), np.arange(top - 1000, top + 1)]))
+        _check_map(hp, k, deltas)
+        # the reference's branchy form (delta >= c_int -> k) agrees on the full range
+        big = np.unique(np.concatenate([deltas[::97], rng.integers(0, dbound + 1, 20000)]))
+        ref = np.where(big >= ci, k, (2 * big * k + ci) // (2 * ci))
+        dp = np.minimum(big, c_eff)
+        mine = (2 * k * dp + c_eff) // (2 * c_eff)
+        assert np.array_equal(ref, mine)
+
+
+def test_use32_holds_for_baseline_configs():
+    """The BASELINE configs (b = 5, d <= 128) always take the exact 32-bit path."""
+    for ci in (614, 716, 5359, 37335, 48161, 58043, 63190, 1 << 52):
+        for d in (64, 128):
+            hp = _lib.softmax_params_host(ci, 2 * d * 127 * 127, 32)
+            assert hp.use32 == 1

@@ -198,3 +198,15 @@ def test_torch_inputs_stay_on_device():
     assert out.is_cuda
     want, _ = O.attention_batched(q, q, q, causal=True)
     assert np.array_equal(out.cpu().numpy().view(np.uint32), want.view(np.uint32))
+
+
+def test_sharded_single_rank_gpu_tensor_scales():
+    """Sharding launcher on one GPU: precomputed (all-reduced) global scales path."""
+    from paper_2511_21513_b200 import sharding
+    rng = np.random.default_rng(21)
+    q = rng.standard_normal((3, 4, 150, 64), dtype=np.float32)
+    k = rng.standard_normal((3, 2, 150, 64), dtype=np.float32)
+    v = rng.standard_normal((3, 2, 150, 64), dtype=np.float32)
+    out, _ = sharding.sharded_attention(q, k, v, causal=True, scale_granularity="tensor")
+    want, _ = O.attention_batched(q, k, v, causal=True, scale_granularity="tensor")
+    assert np.array_equal(out.view(np.uint32), want.view(np.uint32)), _first_diff(out, want)
