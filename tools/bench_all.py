@@ -1,0 +1,93 @@
+"""All five BASELINE configs on one GPU: device time (CUDA events), TOPS,
+tokens/s, and bit-exact check of every (b, head) unit against the reference's
+golden digests.  Writes one JSON line per config (profiles/ summary input).
+
+    python tools/bench_all.py [--configs C1,C2,...] [--iters 10]
+"""
+import argparse
+import json
+import os
+import statistics
+import sys
+
+ROOT = os.path.join(os.path.dirname(os.path.abspath(__file__)), "..")
+sys.path.insert(0, ROOT)
+sys.path.insert(0, os.path.join(ROOT, "tests"))
+
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+
+from cases import digest  # noqa: E402
+from golden_io import configs  # noqa: E402
+from paper_2511_21513_b200 import engine as E  # noqa: E402
+from paper_2511_21513_b200 import workloads  # noqa: E402
+
+
+def run(name, iters):
+    G = configs().get(name)
+    wl = workloads.make("C2" if name == "C2h" else name)
+    gran = "head" if name == "C2h" else wl.scale_granularity
+    B, H, Hkv, L, d = wl.shape
+    dev = torch.device("cuda", 0)
+    q, k, v = (torch.from_numpy(x).to(dev) for x in (wl.q, wl.k, wl.v))
+    sl = None if wl.seq_lens is None else torch.from_numpy(wl.seq_lens).to(dev)
+    out = torch.empty_like(q)
+    lut = E.lut_bytes(5, 6.6)
+
+    class T:
+        def __init__(self):
+            self.ev = {}
+
+        def mark(self, n):
+            e = torch.cuda.Event(enable_timing=True)
+            e.record()
+            self.ev[n] = e
+
+    E.attention(q, k, v, causal=wl.causal, seq_lens=sl, scale_granularity=gran, lut=lut, out=out)
+    for _ in range(3):
+        E.attention(q, k, v, causal=wl.causal, seq_lens=sl, scale_granularity=gran, lut=lut,
+                    out=out, check_finite=False)
+    ts = []
+    for _ in range(iters):
+        t = T()
+        E.attention(q, k, v, causal=wl.causal, seq_lens=sl, scale_granularity=gran, lut=lut,
+                    out=out, check_finite=False, timer=t)
+        ts.append(t)
+    torch.cuda.synchronize()
+    tot = statistics.median(t.ev["start"].elapsed_time(t.ev["attention"]) for t in ts) / 1e3
+    att = statistics.median(t.ev["quantized"].elapsed_time(t.ev["attention"]) for t in ts) / 1e3
+    qnt = statistics.median(t.ev["start"].elapsed_time(t.ev["quantized"]) for t in ts) / 1e3
+    res = out.cpu().numpy()
+    exact = None
+    if G is not None:
+        lens = wl.lengths()
+        bad = 0
+        u = 0
+        for b in range(B):
+            for h in range(H):
+                n = int(lens[b])
+                if digest(res[b, h, :n]) != G["unit_digests"][u] or res[b, h, n:].view(np.uint32).any():
+                    bad += 1
+                u += 1
+        exact = bad == 0
+    ops = wl.ops()
+    qbytes = 5 * (wl.q.size + wl.k.size + wl.v.size)
+    return {"config": name, "shape": [B, H, Hkv, L, d], "causal": wl.causal, "scale": gran,
+            "ms_total": tot * 1e3, "ms_quantize": qnt * 1e3, "ms_fused": att * 1e3,
+            "tops_total": ops / tot / 1e12, "tops_fused": ops / att / 1e12,
+            "tokens_per_s": wl.tokens() / tot, "quantizer_gbs": qbytes / qnt / 1e9,
+            "bit_exact_vs_reference": exact,
+            "ref_cpu_seconds_survey": None if G is None else G.get("ref_seconds")}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--configs", default="C1,C2,C2h,C3,C4,C5")
+    ap.add_argument("--iters", type=int, default=10)
+    a = ap.parse_args()
+    for name in a.configs.split(","):
+        print(json.dumps(run(name, a.iters)), flush=True)
+
+
+if __name__ == "__main__":
+    main()
