@@ -127,6 +127,84 @@ __global__ void quantize_rows_kernel(const float* __restrict__ x, int64_t total_
   }
 }
 
+__device__ __forceinline__ uint32_t q_pack4(float4 v, float s) {
+  return (uint32_t)(uint8_t)q_value(v.x, s) | ((uint32_t)(uint8_t)q_value(v.y, s) << 8) |
+         ((uint32_t)(uint8_t)q_value(v.z, s) << 16) | ((uint32_t)(uint8_t)q_value(v.w, s) << 24);
+}
+
+// Vectorised row-major fast path (ROWS mode, cols % 4 == 0, 16-byte aligned
+// input, out_pitch % 16 == 0): each thread produces one 16-byte output chunk
+// (4 float4 loads -> 16 int8), a row is out_pitch/16 consecutive threads.
+__global__ void __launch_bounds__(256) quantize_rows_vec_kernel(
+    const float* __restrict__ x, int64_t total_rows, int64_t rows_per_group, int cols,
+    const int32_t* __restrict__ valid_rows, int64_t valid_div, int64_t slot_div,
+    const float* __restrict__ scales, int8_t* __restrict__ out, int out_pitch) {
+  const int chunks = out_pitch >> 4;           // 16-byte chunks per row (<= 64)
+  const int rows_per_iter = blockDim.x / chunks;
+  const int lr = threadIdx.x / chunks, ch = threadIdx.x - lr * chunks;
+  if (lr >= rows_per_iter) return;
+  const int c0 = ch << 4;
+  for (int64_t r = (int64_t)blockIdx.x * rows_per_iter + lr; r < total_rows;
+       r += (int64_t)gridDim.x * rows_per_iter) {
+    const int64_t g = r / rows_per_group;
+    bool valid = true;
+    if (valid_rows) valid = (r - g * rows_per_group) < (int64_t)valid_rows[g / valid_div];
+    uint4 o = make_uint4(0u, 0u, 0u, 0u);
+    if (valid && c0 < cols) {
+      const float s = scales[g / slot_div];
+      const float4* xr = reinterpret_cast<const float4*>(x + r * cols + c0);
+      if (c0 + 16 <= cols) {
+        const float4 a = __ldg(xr), b = __ldg(xr + 1), c = __ldg(xr + 2), d = __ldg(xr + 3);
+        o = make_uint4(q_pack4(a, s), q_pack4(b, s), q_pack4(c, s), q_pack4(d, s));
+      } else {
+        uint32_t w[4] = {0u, 0u, 0u, 0u};
+        for (int e = 0; e < 4 && c0 + 4 * e < cols; ++e) w[e] = q_pack4(__ldg(xr + e), s);
+        o = make_uint4(w[0], w[1], w[2], w[3]);
+      }
+    }
+    *reinterpret_cast<uint4*>(out + r * out_pitch + c0) = o;
+  }
+}
+
+// Vectorised V^T fast path: 64 rows x 64 columns per block, float4 loads along
+// the columns, transposed through smem, 16-byte stores along the rows.
+__global__ void __launch_bounds__(256) quantize_rows_t_vec_kernel(
+    const float* __restrict__ x, int rows_per_group, int cols,
+    const int32_t* __restrict__ valid_rows, int64_t valid_div, int64_t slot_div,
+    const float* __restrict__ scales, int8_t* __restrict__ out, int out_pitch, int out_rows,
+    int64_t out_group_stride) {
+  __shared__ uint8_t tile[64][64 + 16];
+  const int64_t g = blockIdx.z;
+  const int r0 = blockIdx.x * 64, c0 = blockIdx.y * 64;
+  int nvalid = rows_per_group;
+  if (valid_rows) {
+    const int v = valid_rows[g / valid_div];
+    nvalid = v < nvalid ? v : nvalid;
+  }
+  const float s = scales[g / slot_div];
+  const float* xg = x + g * (int64_t)rows_per_group * cols;
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {  // 64 rows x 16 float4 = 1024 loads
+    const int t = threadIdx.x + k * 256;
+    const int rr = t >> 4, c4 = (t & 15) << 2;
+    const int r = r0 + rr, c = c0 + c4;
+    uint32_t q = 0;
+    if (r < nvalid && c < cols) q = q_pack4(__ldg(reinterpret_cast<const float4*>(xg + (int64_t)r * cols + c)), s);
+    tile[c4 + 0][rr] = (uint8_t)q;
+    tile[c4 + 1][rr] = (uint8_t)(q >> 8);
+    tile[c4 + 2][rr] = (uint8_t)(q >> 16);
+    tile[c4 + 3][rr] = (uint8_t)(q >> 24);
+  }
+  __syncthreads();
+  const int cc = threadIdx.x >> 2, r16 = (threadIdx.x & 3) << 4;  // 64 cols x 4 chunks of 16 rows
+  const int c = c0 + cc, r = r0 + r16;
+  if (c < out_rows && r < out_pitch) {
+    const uint32_t* tw = reinterpret_cast<const uint32_t*>(&tile[cc][r16]);
+    *reinterpret_cast<uint4*>(out + g * out_group_stride + (int64_t)c * out_pitch + r) =
+        make_uint4(tw[0], tw[1], tw[2], tw[3]);
+  }
+}
+
 // Transposed output per row group: out[g][c][r] (V^T), 64x64 tiles through smem.
 __global__ void quantize_rows_t_kernel(const float* __restrict__ x, int64_t rows_per_group,
                                        int64_t cols, const int32_t* __restrict__ valid_rows,
@@ -236,6 +314,17 @@ extern "C" int ia_quantize(const float* x, int64_t n_rowgroups, int64_t rows_per
     if (out_pitch < cols || (out_pitch & 3) || (((uintptr_t)out) & 3))
       return fail(IA_ERR_INVALID_ARGUMENT, "ia_quantize: out_pitch must be >= cols, %4");
     const int64_t rows = n_rowgroups * rows_per_group;
+    if (mode == IA_QMODE_ROWS && (cols & 3) == 0 && (out_pitch & 15) == 0 && out_pitch <= 1024 &&
+        cols <= 0x7fffffff && (((uintptr_t)x | (uintptr_t)out) & 15) == 0) {
+      const int chunks = (int)(out_pitch >> 4);
+      const int64_t rows_per_block = 256 / chunks;
+      int64_t blocks = (rows + rows_per_block - 1) / rows_per_block;
+      if (blocks > (int64_t)num_sms() * 32) blocks = (int64_t)num_sms() * 32;
+      quantize_rows_vec_kernel<<<(unsigned)blocks, 256, 0, st>>>(
+          x, rows, rows_per_group, (int)cols, valid_rows, valid_div, slot_div, scales, out,
+          (int)out_pitch);
+      return check_launch("quantize_rows_vec_kernel");
+    }
     const int64_t n = rows * (out_pitch >> 2);
     int64_t blocks = (n + 255) / 256;
     if (blocks > (int64_t)num_sms() * 16) blocks = (int64_t)num_sms() * 16;
@@ -250,6 +339,15 @@ extern "C" int ia_quantize(const float* x, int64_t n_rowgroups, int64_t rows_per
   const int64_t out_rows = out_group_stride / out_pitch;
   dim3 grid((unsigned)((rows_per_group + 63) / 64), (unsigned)((out_rows + 63) / 64),
             (unsigned)n_rowgroups);
+  if ((cols & 3) == 0 && (out_pitch & 15) == 0 && (out_group_stride & 15) == 0 &&
+      rows_per_group < 0x7fffffff && out_pitch < 0x7fffffff &&
+      (((uintptr_t)x | (uintptr_t)out) & 15) == 0) {
+    quantize_rows_t_vec_kernel<<<grid, 256, 0, st>>>(x, (int)rows_per_group, (int)cols, valid_rows,
+                                                     valid_div, slot_div, scales, out,
+                                                     (int)out_pitch, (int)out_rows,
+                                                     out_group_stride);
+    return check_launch("quantize_rows_t_vec_kernel");
+  }
   quantize_rows_t_kernel<<<grid, 256, 0, st>>>(x, rows_per_group, cols, valid_rows, valid_div,
                                                slot_div, scales, out, out_pitch,
                                                out_group_stride);
