@@ -93,7 +93,7 @@ typedef struct ia_head_params {
   int32_t use32;    /* 1: the 32-bit magic path is exact for every reachable n */
   float out_scale;
   float s_q, s_k, s_v;
-  int32_t reserved;
+  int32_t unc32;    /* 1: the magic is also exact without the clip (n up to 2k*2*d*127^2 + c_eff) */
 } ia_head_params;
 
 int ia_head_params_host(double c, int64_t d, int nlut, int p_scale, float s_q, float s_k,

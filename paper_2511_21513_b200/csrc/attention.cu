@@ -85,14 +85,17 @@ struct Cfg {
   static_assert(OFF_TAB >= BM * STAGE_PITCH * 4, "epilogue staging must fit in Q/K/V stages");
 };
 
-// Row tables: u32 [nlut][128] (conflict-free gathers) for nlut <= 64, else u8.
+// Row tables: u32 [tab_entries][128] (conflict-free gathers) for nlut <= 64, else u8.
+// For nlut <= 32 the u32 table is zero-extended to 56 entries so warps whose
+// largest reachable index is < 56 can skip the per-logit clip (IdxMap::idx_u).
 __host__ __device__ constexpr bool wide_tab(int nlut) { return nlut <= 64; }
+__host__ __device__ constexpr int tab_entries(int nlut) { return nlut <= 32 ? 56 : nlut; }
 
 template <int DP>
 constexpr size_t attn_smem_bytes(int nlut) {
   return 1024 /* alignment slack */ + (size_t)Cfg<DP>::OFF_TAB +
-         (size_t)nlut * (wide_tab(nlut) ? 512 : 128) /* row tables */ +
-         2 * 3 * 512 /* row exchange */ + 512 /* barriers + tmem slot */;
+         (size_t)tab_entries(nlut) * (wide_tab(nlut) ? 512 : 128) /* row tables */ +
+         3 * 3 * 512 /* row exchange */ + 512 /* barriers + tmem slot */;
 }
 
 // Masked-key bits for one 32-key chunk starting at j0 for query row i
@@ -152,8 +155,10 @@ __global__ void __launch_bounds__(Cfg<DP>::NTHREADS, 1)
   const int nlut = p.nlut;
   const bool wtab = wide_tab(nlut);
   uint8_t* tab = smem + C::OFF_TAB;  // row tables [nlut][128], u32 (wide) or u8 entries
-  int32_t* xmax = reinterpret_cast<int32_t*>(tab + nlut * (wtab ? 512 : 128));  // [NWG][128]
-  uint32_t* xsum = reinterpret_cast<uint32_t*>(xmax + 3 * 128);     // [NWG][128]
+  const int ntab = tab_entries(nlut);
+  int32_t* xmax = reinterpret_cast<int32_t*>(tab + ntab * (wtab ? 512 : 128));  // [NWG][128]
+  int32_t* xmin = xmax + 3 * 128;                                                // [NWG][128]
+  uint32_t* xsum = reinterpret_cast<uint32_t*>(xmin + 3 * 128);                  // [NWG][128]
   uint64_t* bars = reinterpret_cast<uint64_t*>(xsum + 3 * 128);
   uint64_t* q_full = bars;
   uint64_t* k_full = q_full + 1;
@@ -329,15 +334,15 @@ __global__ void __launch_bounds__(Cfg<DP>::NTHREADS, 1)
     // load of the tile, in every pass.
     const bool tm = (threadIdx.x == 128);
     if (tm) IA_TMARK(0);
-    // ---- pass 1: row max over unmasked keys (softmax.py:139-143, :174-179)
-    int32_t mx = INT_MIN;
+    // ---- pass 1: row max over unmasked keys (softmax.py:139-143, :174-179); the row
+    // min rides along (free: pass 1 waits on the MMA) to size the unclipped index range
+    int32_t mx = INT_MIN, mn = INT_MAX;
     for (int n = wg; n < n_kt; n += NWG) {
       long long tw0 = clk64();
       mbar_wait(s_full + wg, s_ph);
       s_ph ^= 1u;
       if (tm) IA_TADD(15, clk64() - tw0);
       tc_fence_after();
-      const bool clean = (n * BN + BN - 1 <= lim) && !p.mask_bits;  // no masked key in tile
 #pragma unroll 1
       for (int hb = 0; hb < BN / 64; ++hb) {
         uint32_t va[32], vb[32];
@@ -355,37 +360,63 @@ __global__ void __launch_bounds__(Cfg<DP>::NTHREADS, 1)
             if (j0 + 32 + e < p.L) dl[32 + e] = (int32_t)vb[e];
           }
         }
-        if (!row_valid) continue;
-        uint32_t ma = 0u, mbb = 0u;
-        if (__builtin_expect(!clean, 0)) {
-          ma = chunk_mask(p, i, j0, lim);
-          mbb = chunk_mask(p, i, j0 + 32, lim);
-        }
-        if ((ma | mbb) == 0) {
+        // Causal / length masking is a per-row cut-off: keys j0 + e with e >= cut are
+        // excluded (cut <= 0: whole batch; invalid rows: cut = 0).  Dense masks take
+        // the bitmask path.
+        const int cut = row_valid ? lim - j0 + 1 : 0;
+        if (!p.mask_bits) {
+          if (!__any_sync(0xffffffffu, cut < 64)) {
 #pragma unroll
-          for (int e = 0; e < 32; e += 2)
-            mx = max(mx, max(max((int32_t)va[e], (int32_t)va[e + 1]),
-                             max((int32_t)vb[e], (int32_t)vb[e + 1])));
-        } else {
+            for (int e = 0; e < 32; e += 2) {
+              mx = max(mx, max(max((int32_t)va[e], (int32_t)va[e + 1]),
+                               max((int32_t)vb[e], (int32_t)vb[e + 1])));
+              mn = min(mn, min(min((int32_t)va[e], (int32_t)va[e + 1]),
+                               min((int32_t)vb[e], (int32_t)vb[e + 1])));
+            }
+          } else {
+#pragma unroll
+            for (int e = 0; e < 32; ++e) {
+              if (e < cut) { mx = max(mx, (int32_t)va[e]); mn = min(mn, (int32_t)va[e]); }
+              if (e + 32 < cut) { mx = max(mx, (int32_t)vb[e]); mn = min(mn, (int32_t)vb[e]); }
+            }
+          }
+        } else if (row_valid) {
+          const uint32_t ma = chunk_mask(p, i, j0, lim), mbb = chunk_mask(p, i, j0 + 32, lim);
 #pragma unroll
           for (int e = 0; e < 32; ++e) {
-            if (!((ma >> e) & 1u)) mx = max(mx, (int32_t)va[e]);
-            if (!((mbb >> e) & 1u)) mx = max(mx, (int32_t)vb[e]);
+            if (!((ma >> e) & 1u)) { mx = max(mx, (int32_t)va[e]); mn = min(mn, (int32_t)va[e]); }
+            if (!((mbb >> e) & 1u)) { mx = max(mx, (int32_t)vb[e]); mn = min(mn, (int32_t)vb[e]); }
           }
         }
       }
     }
     if (tm) IA_TMARK(1);
     xmax[wg * 128 + row] = mx;
+    xmin[wg * 128 + row] = mn;
     named_bar_sync(1, NWT);
     int32_t m = xmax[row];
+    mn = xmin[row];
 #pragma unroll
-    for (int w = 1; w < NWG; ++w) m = max(m, xmax[w * 128 + row]);
+    for (int w = 1; w < NWG; ++w) {
+      m = max(m, xmax[w * 128 + row]);
+      mn = min(mn, xmin[w * 128 + row]);
+    }
     const bool dead = (m == INT_MIN);  // fully masked row: all-zero P^ (softmax.py:181-184)
     if (dead) m = 0;
     const bool fast = hp.use32 != 0;
     IdxMap im;
     im.init(m, hp, k);
+    // Largest index any unmasked logit of this warp's rows can reach without the
+    // clip; if it fits the zero-extended tables, passes 2-3 skip the clip.
+    uint32_t idx_hi = 0;
+    if (row_valid && !dead && hp.unc32) {
+      const int64_t dmax = (int64_t)m - (int64_t)mn;
+      const int64_t hi = (2 * (int64_t)k * dmax + hp.c_eff) / (2 * hp.c_eff);
+      idx_hi = hi > 0x7fffffff ? 0x7fffffffu : (uint32_t)hi;
+    }
+    idx_hi = __reduce_max_sync(0xffffffffu, idx_hi);
+    const bool uncl2 = hp.unc32 && idx_hi < 256u;                      // lut8 has 256 entries
+    const bool uncl3 = hp.unc32 && wtab && idx_hi < (uint32_t)ntab;  // zero-extended row table
 
     // ---- pass 2: idx, e = lut[idx], S = sum e (softmax.py:144-155)
     uint32_t S = 0;
@@ -397,7 +428,6 @@ __global__ void __launch_bounds__(Cfg<DP>::NTHREADS, 1)
         if (tm) IA_TADD(14, clk64() - tw0);
       }
       tc_fence_after();
-      const bool clean = (n * BN + BN - 1 <= lim) && !p.mask_bits;
 #pragma unroll 1
       for (int hb = 0; hb < BN / 64; ++hb) {
         uint32_t va[32], vb[32];
@@ -406,18 +436,31 @@ __global__ void __launch_bounds__(Cfg<DP>::NTHREADS, 1)
           tc_fence_before();
           mbar_arrive(s_free + wg);
         }
-        if (!row_valid || dead || SKEL) continue;
+        if (SKEL) continue;
         const int j0 = n * BN + hb * 64;
-        uint32_t ma = 0u, mbb = 0u;
-        if (__builtin_expect(!clean, 0)) {
-          ma = chunk_mask(p, i, j0, lim);
-          mbb = chunk_mask(p, i, j0 + 32, lim);
-        }
-        if (fast && (ma | mbb) == 0) {
+        // masked keys (e >= cut) take idx = k, lut[k] = 0 (softmax.py:187-188); dead /
+        // invalid rows (cut = 0) sum to S = 0 and get an all-zero table
+        const int cut = (row_valid && !dead) ? lim - j0 + 1 : 0;
+        if (!p.mask_bits && fast) {
+          const bool any_cut = __any_sync(0xffffffffu, cut < 64);
+          if (uncl2 && !any_cut) {
 #pragma unroll
-          for (int e = 0; e < 32; ++e)
-            S += (uint32_t)lut8[im.idx_s((int32_t)va[e])] + (uint32_t)lut8[im.idx_s((int32_t)vb[e])];
-        } else {
+            for (int e = 0; e < 32; ++e)
+              S += (uint32_t)lut8[im.idx_u((int32_t)va[e])] + (uint32_t)lut8[im.idx_u((int32_t)vb[e])];
+          } else if (!any_cut) {
+#pragma unroll
+            for (int e = 0; e < 32; ++e)
+              S += (uint32_t)lut8[im.idx_s((int32_t)va[e])] + (uint32_t)lut8[im.idx_s((int32_t)vb[e])];
+          } else {
+#pragma unroll
+            for (int e = 0; e < 32; ++e) {
+              const uint32_t x0 = e < cut ? im.idx_s((int32_t)va[e]) : k;  // lut8[k] = 0
+              const uint32_t x1 = e + 32 < cut ? im.idx_s((int32_t)vb[e]) : k;
+              S += (uint32_t)lut8[x0] + (uint32_t)lut8[x1];
+            }
+          }
+        } else if (row_valid && !dead) {
+          const uint32_t ma = chunk_mask(p, i, j0, lim), mbb = chunk_mask(p, i, j0 + 32, lim);
 #pragma unroll
           for (int e = 0; e < 32; ++e) {
             if (!((ma >> e) & 1u))
@@ -437,7 +480,7 @@ __global__ void __launch_bounds__(Cfg<DP>::NTHREADS, 1)
     // per-row normalisation table (softmax.py:157-160): (2*scale*lut[t] + S) // (2S)
     {
       const uint32_t two_s = 2u * S;
-      for (int t = wg; t < nlut; t += NWG) {
+      for (int t = wg; t < ntab; t += NWG) {  // t >= nlut: lut8[t] = 0 -> entry 0
         const uint32_t pv = S ? ((uint32_t)p.scale_x2 * lut8[t] + S) / two_s : 0u;
         if (wtab) reinterpret_cast<uint32_t*>(tab)[t * 128 + row] = pv;
         else tab[t * 128 + row] = (uint8_t)pv;
@@ -462,7 +505,6 @@ __global__ void __launch_bounds__(Cfg<DP>::NTHREADS, 1)
         if (tm) IA_TADD(14, clk64() - tw0);
       }
       tc_fence_after();
-      const bool clean = (n * BN + BN - 1 <= lim) && !p.mask_bits;
       const int pbl = tl % C::NPB;
       const uint32_t p_row = p_rows + (uint32_t)(pbl * C::P_BYTES);
       // the P.V that last read this P^ buffer must be done (first use passes at once)
@@ -481,35 +523,49 @@ __global__ void __launch_bounds__(Cfg<DP>::NTHREADS, 1)
         uint32_t pk[16];
 #pragma unroll
         for (int q = 0; q < 16; ++q) pk[q] = 0u;
-        if (row_valid && !dead && !SKEL) {
-          uint32_t ma = 0u, mbb = 0u;
-          if (__builtin_expect(!clean, 0)) {
-            ma = chunk_mask(p, i, j0, lim);
-            mbb = chunk_mask(p, i, j0 + 32, lim);
-          }
-          if (fast && wtab && (ma | mbb) == 0) {
+        const int cut = (row_valid && !dead) ? lim - j0 + 1 : 0;
+        if (SKEL) {
+        } else if (!p.mask_bits && fast && wtab) {
+          const bool any_cut = __any_sync(0xffffffffu, cut < 64);
+          if (uncl3 && !any_cut) {
 #pragma unroll
             for (int q = 0; q < 16; ++q) {
               const uint32_t* v4 = q < 8 ? &va[4 * q] : &vb[4 * (q - 8)];
-              const uint32_t p0 = lds_u32(tab_row + (im.idx_s((int32_t)v4[0]) << 9));
-              const uint32_t p1 = lds_u32(tab_row + (im.idx_s((int32_t)v4[1]) << 9));
-              const uint32_t p2 = lds_u32(tab_row + (im.idx_s((int32_t)v4[2]) << 9));
-              const uint32_t p3 = lds_u32(tab_row + (im.idx_s((int32_t)v4[3]) << 9));
+              const uint32_t p0 = lds_u32(tab_row + (im.idx_u((int32_t)v4[0]) << 9));
+              const uint32_t p1 = lds_u32(tab_row + (im.idx_u((int32_t)v4[1]) << 9));
+              const uint32_t p2 = lds_u32(tab_row + (im.idx_u((int32_t)v4[2]) << 9));
+              const uint32_t p3 = lds_u32(tab_row + (im.idx_u((int32_t)v4[3]) << 9));
               pk[q] = __byte_perm(__byte_perm(p0, p1, 0x0040), __byte_perm(p2, p3, 0x0040), 0x5410);
             }
           } else {
 #pragma unroll
-            for (int e = 0; e < 32; ++e) {
-              const uint32_t xa = ((ma >> e) & 1u) ? k
-                                  : fast ? im.idx((int32_t)va[e])
-                                         : idx_slow(m, (int32_t)va[e], hp.c_eff, k);
-              const uint32_t xb = ((mbb >> e) & 1u) ? k
-                                  : fast ? im.idx((int32_t)vb[e])
-                                         : idx_slow(m, (int32_t)vb[e], hp.c_eff, k);
-              const uint32_t aa = tab_row + (xa << tab_sh), ab = tab_row + (xb << tab_sh);
-              pk[e >> 2] |= (wtab ? lds_u32(aa) : lds_u8(aa)) << (8 * (e & 3));
-              pk[8 + (e >> 2)] |= (wtab ? lds_u32(ab) : lds_u8(ab)) << (8 * (e & 3));
+            for (int q = 0; q < 16; ++q) {
+              const uint32_t* v4 = q < 8 ? &va[4 * q] : &vb[4 * (q - 8)];
+              const int eb = 4 * q;  // masked keys select table entry k (= 0)
+              const uint32_t x0 = eb + 0 < cut ? im.idx_s((int32_t)v4[0]) : k;
+              const uint32_t x1 = eb + 1 < cut ? im.idx_s((int32_t)v4[1]) : k;
+              const uint32_t x2 = eb + 2 < cut ? im.idx_s((int32_t)v4[2]) : k;
+              const uint32_t x3 = eb + 3 < cut ? im.idx_s((int32_t)v4[3]) : k;
+              const uint32_t p0 = lds_u32(tab_row + (x0 << 9));
+              const uint32_t p1 = lds_u32(tab_row + (x1 << 9));
+              const uint32_t p2 = lds_u32(tab_row + (x2 << 9));
+              const uint32_t p3 = lds_u32(tab_row + (x3 << 9));
+              pk[q] = __byte_perm(__byte_perm(p0, p1, 0x0040), __byte_perm(p2, p3, 0x0040), 0x5410);
             }
+          }
+        } else if (row_valid && !dead) {
+          const uint32_t ma = chunk_mask(p, i, j0, lim), mbb = chunk_mask(p, i, j0 + 32, lim);
+#pragma unroll
+          for (int e = 0; e < 32; ++e) {
+            const uint32_t xa = ((ma >> e) & 1u) ? k
+                                : fast ? im.idx((int32_t)va[e])
+                                       : idx_slow(m, (int32_t)va[e], hp.c_eff, k);
+            const uint32_t xb = ((mbb >> e) & 1u) ? k
+                                : fast ? im.idx((int32_t)vb[e])
+                                       : idx_slow(m, (int32_t)vb[e], hp.c_eff, k);
+            const uint32_t aa = tab_row + (xa << tab_sh), ab = tab_row + (xb << tab_sh);
+            pk[e >> 2] |= (wtab ? lds_u32(aa) : lds_u8(aa)) << (8 * (e & 3));
+            pk[8 + (e >> 2)] |= (wtab ? lds_u32(ab) : lds_u8(ab)) << (8 * (e & 3));
           }
         }
         if (DEBUG && p.dbg_prob && i < p.L) {

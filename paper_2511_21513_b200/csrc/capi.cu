@@ -123,7 +123,6 @@ extern "C" int ia_softmax_params_host(int64_t c_int, int64_t delta_bound, int nl
   fill_head_params(c_int < kCIntCap ? c_int : kCIntCap, delta_bound, nlut, out);
   out->out_scale = 0.0f;
   out->s_q = out->s_k = out->s_v = 0.0f;
-  out->reserved = 0;
   return IA_OK;
 }
 

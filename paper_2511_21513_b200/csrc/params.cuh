@@ -46,6 +46,10 @@ __host__ __device__ inline int bitlen_u64(uint64_t x) {
 // n*M / 2^(32+s) = n/D + n*e/(D 2^(32+s)) and n*e < n_max*D <= 2^(32+s), so the
 // error term is below 1/D and floor(n*M / 2^(32+s)) = floor(n / D).
 // use32 requires n_max < 2^31 (then M < 2^32); else the kernels divide in 64-bit.
+// When the UNCLAMPED range 2k*dbound + c_eff is also below 2^31 the magic is
+// derived for it instead (unc32 = 1): idx = floor(n / D) is then exact for every
+// reachable delta without the clip, so a kernel that knows its rows' largest
+// delta can drop the per-element min() and read a zero-extended table instead.
 // dbound: an upper bound on delta = m - a over the logits this map will see
 // (2*d*127^2 for int8 operands; 2^32 - 1 for arbitrary int32 logits).
 __host__ __device__ inline void fill_head_params(int64_t c_int, int64_t dbound, int nlut,
@@ -53,9 +57,15 @@ __host__ __device__ inline void fill_head_params(int64_t c_int, int64_t dbound, 
   const int64_t k = nlut - 1;
   const int64_t clamp = 2 * k * dbound + 1;
   const int64_t c_eff = c_int < clamp ? c_int : clamp;
-  int64_t n_max = 2 * k * dbound + c_eff;
+  const int64_t n_unc = 2 * k * dbound + c_eff;  // largest n without the clip
+  int64_t n_max = n_unc;
   const int64_t alt = (2 * k + 1) * c_eff;
   if (alt < n_max) n_max = alt;
+  hp->unc32 = 0;
+  if (n_unc < (int64_t(1) << 31)) {
+    n_max = n_unc;
+    hp->unc32 = 1;
+  }
   hp->c_int = c_int;
   hp->c_eff = c_eff;
   hp->use32 = 0;
@@ -74,6 +84,7 @@ __host__ __device__ inline void fill_head_params(int64_t c_int, int64_t dbound, 
       hp->shift = s;
     }
   }
+  if (!hp->use32) hp->unc32 = 0;
 }
 
 __host__ __device__ inline void make_head_params(double c, int64_t d, int nlut, int p_scale,
@@ -84,7 +95,6 @@ __host__ __device__ inline void make_head_params(double c, int64_t d, int nlut, 
   hp->s_q = s_q;
   hp->s_k = s_k;
   hp->s_v = s_v;
-  hp->reserved = 0;
 }
 
 #ifdef __CUDACC__
@@ -120,6 +130,12 @@ struct IdxMap {
   __device__ __forceinline__ uint32_t idx_s(int32_t a) const {
     const int32_t ac = max(a, lo);
     const uint32_t n = base + nk2 * (uint32_t)ac;
+    return __umulhi(n, magic) >> shift;
+  }
+  // Unclamped (hp.unc32): floor((2k*delta + c_eff) / (2 c_eff)) for any reachable
+  // delta; may exceed k, callers index a table zero-extended past k.
+  __device__ __forceinline__ uint32_t idx_u(int32_t a) const {
+    const uint32_t n = base + nk2 * (uint32_t)a;
     return __umulhi(n, magic) >> shift;
   }
 };

@@ -100,6 +100,13 @@ def test_magic_index_map_exhaustive(b, d):
             deltas = np.unique(np.concatenate([rng.integers(0, top + 1, 2_000_000),
                                                np.arange(0, 1000), np.arange(top - 1000, top + 1)]))
         _check_map(hp, k, deltas)
+        if hp.unc32:  # the same magic is exact without the clip, up to delta = dbound
+            un = np.unique(np.concatenate([rng.integers(0, dbound + 1, 400000),
+                                           np.arange(max(0, dbound - 2000), dbound + 1)]))
+            n_u = (2 * k * un + c_eff).astype(np.uint64)
+            assert int(n_u.max()) < (1 << 31)
+            got = ((n_u * np.uint64(hp.magic)) >> np.uint64(32)) >> np.uint64(hp.shift)
+            assert np.array_equal(got, n_u // np.uint64(2 * c_eff))
         # the reference's branchy form (delta >= c_int -> k) agrees on the full range
         big = np.unique(np.concatenate([deltas[::97], rng.integers(0, dbound + 1, 20000)]))
         ref = np.where(big >= ci, k, (2 * big * k + ci) // (2 * ci))
@@ -113,4 +120,4 @@ def test_use32_holds_for_baseline_configs():
     for ci in (614, 716, 5359, 37335, 48161, 58043, 63190, 1 << 52):
         for d in (64, 128):
             hp = _lib.softmax_params_host(ci, 2 * d * 127 * 127, 32)
-            assert hp.use32 == 1
+            assert hp.use32 == 1 and hp.unc32 == 1
