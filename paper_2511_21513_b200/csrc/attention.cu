@@ -53,6 +53,7 @@ struct AttnDev {
   long long* dbg_times;  // optional per-CTA phase clocks (development instrumentation)
   int B, H, Hkv, L, d, mask_words;
   int causal, nlut, scale_x2, n_qt;
+  int xflags;  // development experiments (IA_XFLAGS); 0 in production
   uint8_t lut[256];
 };
 
@@ -80,7 +81,18 @@ struct Cfg {
   static constexpr int NPB = DP <= 128 ? 2 : 1;  // P^ buffers per softmax warpgroup
   static constexpr int OFF_P = OFF_V + NVST * V_BYTES;
   static constexpr int OFF_TAB = OFF_P + NWG * NPB * P_BYTES;
+  // During passes 1-2 the P^ area is idle, so the K ring borrows it: NKX stages
+  // (the NKST regular ones first) instead of NKST.  Pass-3 loads use only the
+  // regular stages; every pass-2 QK^T has completed (its S tile was read) before
+  // any warpgroup leaves the pass-2 row-sum exchange and writes a P^ tile.
+  static constexpr int NKX_RAW = NKST + (NWG * NPB * P_BYTES) / K_BYTES;
+  static constexpr int NKX = NKX_RAW > 16 ? 16 : NKX_RAW;
   static constexpr int KSTEPS = DP / 32;
+  static constexpr int BAR_BYTES = 8 * (1 + 2 * NKX + 2 * NVST + 2 * NWG + 2 * NWG * NPB + 1) + 4;
+  static_assert(BAR_BYTES <= 512, "barrier block");
+  __host__ __device__ static constexpr int k_off(int s) {
+    return s < NKST ? OFF_K + s * K_BYTES : OFF_P + (s - NKST) * K_BYTES;
+  }
   static constexpr int STAGE_PITCH = DP + 1;  // f32 epilogue staging row pitch (words, conflict-free)
   static_assert(OFF_TAB >= BM * STAGE_PITCH * 4, "epilogue staging must fit in Q/K/V stages");
 };
@@ -95,7 +107,7 @@ template <int DP>
 constexpr size_t attn_smem_bytes(int nlut) {
   return 1024 /* alignment slack */ + (size_t)Cfg<DP>::OFF_TAB +
          (size_t)tab_entries(nlut) * (wide_tab(nlut) ? 512 : 128) /* row tables */ +
-         3 * 3 * 512 /* row exchange */ + 512 /* barriers + tmem slot */;
+         3 * 3 * 512 /* row exchange */ + 512 /* barriers + tmem slot (Cfg::BAR_BYTES) */;
 }
 
 // Masked-key bits for one 32-key chunk starting at j0 for query row i
@@ -136,9 +148,22 @@ __device__ __forceinline__ long long clk64() {
   do {                                                                                      \
     if (IA_PROFILE && p.dbg_times) p.dbg_times[(size_t)blockIdx.x * 16 + (slot)] = clk64(); \
   } while (0)
-#define IA_TADD(slot, v)                                                                    \
-  do {                                                                                      \
-    if (IA_PROFILE && p.dbg_times) p.dbg_times[(size_t)blockIdx.x * 16 + (slot)] += (v);    \
+// Event timeline of two CTAs (0 and IA_TRACE_CTA2): per-role segments of 2048
+// entries after the per-CTA slots, entry = clock << 16 | event << 12 | tile.
+#define IA_TRACE_CTA2 1000
+#define IA_TRACE(seg, ev, t)                                                                  \
+  do {                                                                                        \
+    if (IA_PROFILE && p.dbg_times && (blockIdx.x == 0 || blockIdx.x == IA_TRACE_CTA2)) {      \
+      long long* tb_ = p.dbg_times + (size_t)gridDim.x * 16 +                                 \
+                       ((blockIdx.x ? 7 : 0) + (seg)) * 2048;                                 \
+      tb_[trc++ & 2047] = (clk64() << 16) | ((long long)(ev) << 12) | ((t) & 0xfff);          \
+    }                                                                                         \
+  } while (0)
+// Wait-time accumulators live in registers (tacc) and are flushed once at the end,
+// so the instrumentation adds no global round trips to the pipeline loops.
+#define IA_TADD(slot, v)              \
+  do {                                \
+    if (IA_PROFILE) tacc[(slot)-8] += (v); \
   } while (0)
 
 template <int DP, bool DEBUG, bool SKEL = false>
@@ -162,8 +187,8 @@ __global__ void __launch_bounds__(Cfg<DP>::NTHREADS, 1)
   uint64_t* bars = reinterpret_cast<uint64_t*>(xsum + 3 * 128);
   uint64_t* q_full = bars;
   uint64_t* k_full = q_full + 1;
-  uint64_t* k_empty = k_full + C::NKST;
-  uint64_t* v_full = k_empty + C::NKST;
+  uint64_t* k_empty = k_full + C::NKX;
+  uint64_t* v_full = k_empty + C::NKX;
   uint64_t* v_empty = v_full + C::NVST;
   uint64_t* s_full = v_empty + C::NVST;       // [NWG] QK issuer -> softmax (QK^T landed in S[w])
   uint64_t* s_free = s_full + NWG;         // [NWG] softmax -> QK issuer (S[w] fully read)
@@ -191,13 +216,15 @@ __global__ void __launch_bounds__(Cfg<DP>::NTHREADS, 1)
   const int key_end = p.causal ? min(q0 + BM, len) : len;
   const int n_kt = (key_end + BN - 1) / BN;
   const bool resident = n_kt <= NWG;  // every logit tile fits its own TMEM buffer
+  const int npass = resident ? 1 : ((p.xflags & 1) ? 1 : 3);
+  const int n_kt_b = (p.xflags & 1) ? 0 : n_kt;  // key tiles of passes 2-3 / P.V
 
   if (warp == 0 && lane == 0) {
     prefetch_tmap(&tmq);
     prefetch_tmap(&tmk);
     prefetch_tmap(&tmv);
     mbar_init(q_full, 1);
-    for (int s = 0; s < C::NKST; ++s) { mbar_init(k_full + s, 1); mbar_init(k_empty + s, 1); }
+    for (int s = 0; s < C::NKX; ++s) { mbar_init(k_full + s, 1); mbar_init(k_empty + s, 1); }
     for (int s = 0; s < C::NVST; ++s) { mbar_init(v_full + s, 1); mbar_init(v_empty + s, 1); }
     for (int w = 0; w < NWG; ++w) {
       mbar_init(s_full + w, 1);
@@ -219,101 +246,138 @@ __global__ void __launch_bounds__(Cfg<DP>::NTHREADS, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
+  int trc = 0;  // trace entry counter (IA_TRACE)
+  (void)trc;
+  long long tacc[8] = {0, 0, 0, 0, 0, 0, 0, 0};  // IA_TADD slots 8..15
+  (void)tacc;
 
-  // Four single-thread roles: K producer (warp 0), QK^T issuer (warp 1), V^T
-  // producer (warp 2, after the TMEM allocation), P.V issuer (warp 3).  Keeping
-  // the two MMA streams in separate threads lets QK^T(n + NWG) start as soon as
-  // S[w] is read back, independent of P.V(n) progress.
+  // Four role warps: K producer (warp 0), QK^T issuer (warp 1), V^T producer
+  // (warp 2, after the TMEM allocation), P.V issuer (warp 3).  Each role loop runs
+  // warp-wide (the waits on every lane, the TMA / MMA issue on one elected lane),
+  // with the smem descriptors precomputed: the issue loops sit on the pipeline's
+  // critical path, and a lone-lane loop with per-iteration descriptor math was
+  // measured to cost ~1000 cycles per tile.  Keeping the two MMA streams in
+  // separate warps lets QK^T(n + NWG) start as soon as S[w] is read back,
+  // independent of P.V(n) progress.
   if (warp == 0) {
     // ------------------------------------------------------------ K producer (+ Q)
-    if (lane == 0) {
+    if (elect_one()) {
       mbar_expect_tx(q_full, C::Q_BYTES);
       for (int s = 0; s < C::NSUB; ++s)
         tma_load_3d(smem + C::OFF_Q + s * C::SUB_BYTES, &tmq, q_full, s * C::SW, q0, bh);
-      int ks = 0, kph = 0;
-      const int nloads = (resident ? 1 : 3) * n_kt;
-      for (int t = 0; t < nloads; ++t) {
-        const int n = t % n_kt;
-        mbar_wait(k_empty + ks, kph ^ 1);
+    }
+    __syncwarp();
+    uint32_t kph = 0;  // per-stage phase bits
+    int n = 0, ks = 0;
+    const int t3 = 2 * n_kt;
+    const int nloads = npass * n_kt;
+    for (int t = 0; t < nloads; ++t) {
+      mbar_wait(k_empty + ks, ((kph >> ks) & 1u) ^ 1u);
+      kph ^= 1u << ks;
+      if (elect_one()) {
+        IA_TRACE(0, 1, t);
         mbar_expect_tx(k_full + ks, C::K_BYTES);
         for (int s = 0; s < C::NSUB; ++s)
-          tma_load_3d(smem + C::OFF_K + ks * C::K_BYTES + s * C::SUB_BYTES, &tmk, k_full + ks,
-                      s * C::SW, n * BN, kvh);
-        if (++ks == C::NKST) { ks = 0; kph ^= 1; }
+          tma_load_3d(smem + C::k_off(ks) + s * C::SUB_BYTES, &tmk, k_full + ks, s * C::SW,
+                      n * BN, kvh);
       }
+      __syncwarp();
+      if (++n == n_kt) n = 0;
+      ++ks;
+      if (t + 1 < t3 ? ks == C::NKX : ks == C::NKST) ks = 0;
+      if (t + 1 == t3) ks = 0;
     }
   } else if (warp == 2) {
     // ------------------------------------------------------------ V^T producer
-    if (lane == 0) {
-      int vs = 0, vph = 0;
-      for (int n = 0; n < n_kt; ++n) {
-        mbar_wait(v_empty + vs, vph ^ 1);
+    int vs = 0, vph = 0;
+    for (int n = 0; n < n_kt_b; ++n) {
+      mbar_wait(v_empty + vs, vph ^ 1);
+      if (elect_one()) {
+        IA_TRACE(2, 5, n);
         mbar_expect_tx(v_full + vs, C::V_BYTES);
         tma_load_3d(smem + C::OFF_V + vs * C::V_BYTES, &tmv, v_full + vs, n * BN, 0, kvh);
-        if (++vs == C::NVST) { vs = 0; vph ^= 1; }
       }
+      __syncwarp();
+      if (++vs == C::NVST) { vs = 0; vph ^= 1; }
     }
   } else if (warp == 1) {
     // ------------------------------------------------------------ QK^T issuer
     // Tile n of every pass lives in TMEM buffer / warpgroup w = n % NWG.
-    if (lane == 0) {
-      constexpr uint32_t idq = idesc_i8(BM, BN, true, true);  // s8 x s8 -> s32
-      const uint32_t sq = smem_u32(smem + C::OFF_Q);
-      mbar_wait(q_full, 0);
-      int ks = 0, kph = 0;
-      uint32_t used = 0, c_s = 0;  // per-buffer occupied bit / s_free phase
-      const int nmma = (resident ? 1 : 3) * n_kt;
-      for (int t = 0; t < nmma; ++t) {
-        const int w = (t % n_kt) % NWG;
-        long long t0 = clk64();
-        if ((used >> w) & 1u) { mbar_wait(s_free + w, (c_s >> w) & 1u); c_s ^= 1u << w; }
-        used |= 1u << w;
-        long long t1 = clk64();
-        mbar_wait(k_full + ks, kph);
-        long long t2 = clk64();
-        IA_TADD(8, t1 - t0);
-        IA_TADD(9, t2 - t1);
-        tc_fence_after();
-        const uint32_t sk = smem_u32(smem + C::OFF_K + ks * C::K_BYTES);
+    constexpr uint32_t idq = idesc_i8(BM, BN, true, true);  // s8 x s8 -> s32
+    const uint64_t dq = sdesc(smem_u32(smem + C::OFF_Q), C::SBO, C::LAYOUT);
+    const uint64_t d0 = sdesc(smem_u32(smem), C::SBO, C::LAYOUT);  // + (offset >> 4)
+    mbar_wait(q_full, 0);
+    uint32_t kph = 0;            // per-stage K phase bits
+    uint32_t used = 0, c_s = 0;  // per-buffer occupied bit / s_free phase
+    int w = 0, n = 0, ks = 0;
+    const int t3 = 2 * n_kt;
+    const int nmma = npass * n_kt;
+    for (int t = 0; t < nmma; ++t) {
+      long long t0 = clk64();
+      if ((used >> w) & 1u) {
+        mbar_wait(s_free + w, (c_s >> w) & 1u);
+        c_s ^= 1u << w;
+      }
+      used |= 1u << w;
+      long long t1 = clk64();
+      mbar_wait(k_full + ks, (kph >> ks) & 1u);
+      kph ^= 1u << ks;
+      long long t2 = clk64();
+      IA_TADD(8, t1 - t0);
+      IA_TADD(9, t2 - t1);
+      tc_fence_after();
+      if (elect_one()) {
+        IA_TRACE(1, 3, t);
+        const uint64_t dk = d0 + (uint64_t)(C::k_off(ks) >> 4);
+        const uint32_t dt = tmem + (uint32_t)w * 128u;
 #pragma unroll
         for (int kk = 0; kk < C::KSTEPS; ++kk) {
           const uint32_t off = (kk * 32 / C::SW) * C::SUB_BYTES + (kk * 32) % C::SW;
-          mma_i8_ss(tmem + w * 128, sdesc(sq + off, C::SBO, C::LAYOUT),
-                    sdesc(sk + off, C::SBO, C::LAYOUT), idq, kk > 0);
+          mma_i8_ss(dt, dq + (off >> 4), dk + (off >> 4), idq, kk > 0);
         }
         tc_commit(k_empty + ks);
         tc_commit(s_full + w);
-        if (++ks == C::NKST) { ks = 0; kph ^= 1; }
+        IA_TRACE(1, 4, t);
       }
+      __syncwarp();
+      if (++w == NWG) w = 0;
+      if (++n == n_kt) { n = 0; w = 0; }
+      ++ks;
+      if (t + 1 < t3 ? ks == C::NKX : ks == C::NKST) ks = 0;
+      if (t + 1 == t3) ks = 0;
     }
   } else if (warp == 3) {
     // ------------------------------------------------------------ P.V issuer
-    if (lane == 0) {
-      constexpr uint32_t idv = idesc_i8(BM, DP, false, true);  // u8 x s8 -> s32
-      int vs = 0, vph = 0;
-      for (int n = 0; n < n_kt; ++n) {
-        const int w = n % NWG, tl = n / NWG;  // warpgroup and its local tile counter
-        const int pb = w * C::NPB + tl % C::NPB;
-        long long t0 = clk64();
-        mbar_wait(p_full + pb, (uint32_t)(tl / C::NPB) & 1u);
-        long long t1 = clk64();
-        mbar_wait(v_full + vs, vph);
-        long long t2 = clk64();
-        IA_TADD(11, t1 - t0);
-        IA_TADD(12, t2 - t1);
-        tc_fence_after();
-        const uint32_t sp = smem_u32(smem + C::OFF_P + pb * C::P_BYTES);
-        const uint32_t sv = smem_u32(smem + C::OFF_V + vs * C::V_BYTES);
+    constexpr uint32_t idv = idesc_i8(BM, DP, false, true);  // u8 x s8 -> s32
+    const uint64_t dp0 = sdesc(smem_u32(smem + C::OFF_P), 1024, 2u);
+    const uint64_t dv0 = sdesc(smem_u32(smem + C::OFF_V), 1024, 2u);
+    int vs = 0, vph = 0, w = 0, tl = 0;  // warpgroup w's local tile counter tl
+    for (int n = 0; n < n_kt_b; ++n) {
+      const int pb = w * C::NPB + tl % C::NPB;
+      long long t0 = clk64();
+      mbar_wait(p_full + pb, (uint32_t)(tl / C::NPB) & 1u);
+      long long t1 = clk64();
+      mbar_wait(v_full + vs, vph);
+      long long t2 = clk64();
+      IA_TADD(11, t1 - t0);
+      IA_TADD(12, t2 - t1);
+      tc_fence_after();
+      if (elect_one()) {
+        IA_TRACE(3, 7, n);
+        const uint64_t dp = dp0 + (uint64_t)((pb * C::P_BYTES) >> 4);
+        const uint64_t dv = dv0 + (uint64_t)((vs * C::V_BYTES) >> 4);
 #pragma unroll
         for (int kk = 0; kk < BN / 32; ++kk)
-          mma_i8_ss(tmem + C::O_COL, sdesc(sp + kk * 32, 1024, 2u), sdesc(sv + kk * 32, 1024, 2u),
-                    idv, (n > 0 || kk > 0) ? 1u : 0u);
+          mma_i8_ss(tmem + C::O_COL, dp + 2 * kk, dv + 2 * kk, idv, (n > 0 || kk > 0) ? 1u : 0u);
         tc_commit(v_empty + vs);
         tc_commit(p_free + pb);
-        if (++vs == C::NVST) { vs = 0; vph ^= 1; }
       }
-      tc_commit(o_full);
+      __syncwarp();
+      if (++vs == C::NVST) { vs = 0; vph ^= 1; }
+      if (++w == NWG) { w = 0; ++tl; }
     }
+    if (elect_one()) tc_commit(o_full);
+    __syncwarp();
   } else if (warp >= 4) {
     // ------------------------------------------------------------ IndexSoftmax warpgroups
     const int wg = (warp - 4) >> 2;
@@ -333,6 +397,7 @@ __global__ void __launch_bounds__(Cfg<DP>::NTHREADS, 1)
     // flight per wait); S[w] is handed back to the MMA warp right after the last
     // load of the tile, in every pass.
     const bool tm = (threadIdx.x == 128);
+    const bool trw = IA_PROFILE && ((threadIdx.x & 127) == 0);
     if (tm) IA_TMARK(0);
     // ---- pass 1: row max over unmasked keys (softmax.py:139-143, :174-179); the row
     // min rides along (free: pass 1 waits on the MMA) to size the unclipped index range
@@ -340,6 +405,7 @@ __global__ void __launch_bounds__(Cfg<DP>::NTHREADS, 1)
     for (int n = wg; n < n_kt; n += NWG) {
       long long tw0 = clk64();
       mbar_wait(s_full + wg, s_ph);
+      if (trw) IA_TRACE(4 + wg, 8, 0 * n_kt + n);
       s_ph ^= 1u;
       if (tm) IA_TADD(15, clk64() - tw0);
       tc_fence_after();
@@ -350,6 +416,7 @@ __global__ void __launch_bounds__(Cfg<DP>::NTHREADS, 1)
         if (hb == BN / 64 - 1 && !resident) {
           tc_fence_before();
           mbar_arrive(s_free + wg);
+          if (trw) IA_TRACE(4 + wg, 9, 0 * n_kt + n);
         }
         const int j0 = n * BN + hb * 64;
         if (DEBUG && p.dbg_logits && i < p.L) {
@@ -364,7 +431,8 @@ __global__ void __launch_bounds__(Cfg<DP>::NTHREADS, 1)
         // excluded (cut <= 0: whole batch; invalid rows: cut = 0).  Dense masks take
         // the bitmask path.
         const int cut = row_valid ? lim - j0 + 1 : 0;
-        if (!p.mask_bits) {
+        if (p.xflags & 32) {  // experiment: no pass-1 arithmetic
+        } else if (!p.mask_bits) {
           if (!__any_sync(0xffffffffu, cut < 64)) {
 #pragma unroll
             for (int e = 0; e < 32; e += 2) {
@@ -420,10 +488,11 @@ __global__ void __launch_bounds__(Cfg<DP>::NTHREADS, 1)
 
     // ---- pass 2: idx, e = lut[idx], S = sum e (softmax.py:144-155)
     uint32_t S = 0;
-    for (int n = wg; n < n_kt; n += NWG) {
+    for (int n = wg; n < n_kt_b; n += NWG) {
       if (!resident) {
         long long tw0 = clk64();
         mbar_wait(s_full + wg, s_ph);
+        if (trw) IA_TRACE(4 + wg, 8, 1 * n_kt + n);
         s_ph ^= 1u;
         if (tm) IA_TADD(14, clk64() - tw0);
       }
@@ -435,6 +504,7 @@ __global__ void __launch_bounds__(Cfg<DP>::NTHREADS, 1)
         if (hb == BN / 64 - 1 && !resident) {
           tc_fence_before();
           mbar_arrive(s_free + wg);
+          if (trw) IA_TRACE(4 + wg, 9, 1 * n_kt + n);
         }
         if (SKEL) continue;
         const int j0 = n * BN + hb * 64;
@@ -497,10 +567,11 @@ __global__ void __launch_bounds__(Cfg<DP>::NTHREADS, 1)
     int tl = 0;  // this warpgroup's local pass-3 tile counter
 
     // ---- pass 3: P^ = rowtab[idx] -> smem -> P.V MMA (softmax.py:161-162)
-    for (int n = wg; n < n_kt; n += NWG) {
+    for (int n = wg; n < n_kt_b; n += NWG) {
       if (!resident) {
         long long tw0 = clk64();
         mbar_wait(s_full + wg, s_ph);
+        if (trw) IA_TRACE(4 + wg, 8, 2 * n_kt + n);
         s_ph ^= 1u;
         if (tm) IA_TADD(14, clk64() - tw0);
       }
@@ -510,6 +581,7 @@ __global__ void __launch_bounds__(Cfg<DP>::NTHREADS, 1)
       // the P.V that last read this P^ buffer must be done (first use passes at once)
       long long tq0 = clk64();
       mbar_wait(p_free + wg * C::NPB + pbl, ((uint32_t)(tl / C::NPB) & 1u) ^ 1u);
+      if (trw) IA_TRACE(4 + wg, 10, 2 * n_kt + n);
       if (tm) IA_TADD(13, clk64() - tq0);
 #pragma unroll 1
       for (int hb = 0; hb < BN / 64; ++hb) {
@@ -518,6 +590,7 @@ __global__ void __launch_bounds__(Cfg<DP>::NTHREADS, 1)
         if (hb == BN / 64 - 1 && !resident) {
           tc_fence_before();
           mbar_arrive(s_free + wg);
+          if (trw) IA_TRACE(4 + wg, 9, 2 * n_kt + n);
         }
         const int j0 = n * BN + hb * 64;
         uint32_t pk[16];
@@ -582,6 +655,7 @@ __global__ void __launch_bounds__(Cfg<DP>::NTHREADS, 1)
       }
       fence_proxy_async_smem();
       mbar_arrive(p_full + wg * C::NPB + pbl);
+      if (trw) IA_TRACE(4 + wg, 11, 2 * n_kt + n);
       ++tl;
     }
 
@@ -626,6 +700,11 @@ __global__ void __launch_bounds__(Cfg<DP>::NTHREADS, 1)
     }
   }
 
+  if (IA_PROFILE && p.dbg_times) {
+#pragma unroll
+    for (int s = 0; s < 8; ++s)
+      if (tacc[s]) p.dbg_times[(size_t)blockIdx.x * 16 + 8 + s] = tacc[s];
+  }
   tc_fence_before();
   __syncthreads();
   if (threadIdx.x == 0) { IA_TMARK(5); if (IA_PROFILE && p.dbg_times) p.dbg_times[(size_t)blockIdx.x * 16 + 10] = n_kt; }
@@ -681,6 +760,8 @@ static int launch_attn(const ia_attn_args* a, cudaStream_t st) {
   dv.nlut = a->nlut;
   dv.scale_x2 = 2 * a->p_scale;
   dv.n_qt = (int)((a->L + BM - 1) / BM);
+  static const int xflags = getenv("IA_XFLAGS") ? atoi(getenv("IA_XFLAGS")) : 0;
+  dv.xflags = xflags;
   for (int t = 0; t < 256; ++t) dv.lut[t] = t < a->nlut ? a->lut[t] : 0;
   size_t smem = attn_smem_bytes<DP>(a->nlut);
   if (smem < 120 * 1024) smem = 120 * 1024;  // one CTA per SM (it owns all 512 TMEM columns)
