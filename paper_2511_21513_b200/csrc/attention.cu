@@ -155,7 +155,7 @@ __device__ __forceinline__ long long clk64() {
   do {                                                                                        \
     if (IA_PROFILE && p.dbg_times && (blockIdx.x == 0 || blockIdx.x == IA_TRACE_CTA2)) {      \
       long long* tb_ = p.dbg_times + (size_t)gridDim.x * 16 +                                 \
-                       ((blockIdx.x ? 7 : 0) + (seg)) * 2048;                                 \
+                       ((blockIdx.x ? 16 : 0) + (seg)) * 2048;                                 \
       tb_[trc++ & 2047] = (clk64() << 16) | ((long long)(ev) << 12) | ((t) & 0xfff);          \
     }                                                                                         \
   } while (0)
@@ -165,6 +165,12 @@ __device__ __forceinline__ long long clk64() {
   do {                                \
     if (IA_PROFILE) tacc[(slot)-8] += (v); \
   } while (0)
+
+// Barrier wait with the suspend hint (default) or a pure poll (spin = true).
+__device__ __forceinline__ void bwait(uint64_t* bar, uint32_t parity, bool spin) {
+  if (spin) mbar_wait_spin(bar, parity);
+  else mbar_wait(bar, parity);
+}
 
 template <int DP, bool DEBUG, bool SKEL = false>
 __global__ void __launch_bounds__(Cfg<DP>::NTHREADS, 1)
@@ -272,7 +278,7 @@ __global__ void __launch_bounds__(Cfg<DP>::NTHREADS, 1)
     const int t3 = 2 * n_kt;
     const int nloads = npass * n_kt;
     for (int t = 0; t < nloads; ++t) {
-      mbar_wait(k_empty + ks, ((kph >> ks) & 1u) ^ 1u);
+      bwait(k_empty + ks, ((kph >> ks) & 1u) ^ 1u, p.xflags & 16);
       kph ^= 1u << ks;
       if (elect_one()) {
         IA_TRACE(0, 1, t);
@@ -291,7 +297,7 @@ __global__ void __launch_bounds__(Cfg<DP>::NTHREADS, 1)
     // ------------------------------------------------------------ V^T producer
     int vs = 0, vph = 0;
     for (int n = 0; n < n_kt_b; ++n) {
-      mbar_wait(v_empty + vs, vph ^ 1);
+      bwait(v_empty + vs, vph ^ 1, p.xflags & 16);
       if (elect_one()) {
         IA_TRACE(2, 5, n);
         mbar_expect_tx(v_full + vs, C::V_BYTES);
@@ -315,12 +321,12 @@ __global__ void __launch_bounds__(Cfg<DP>::NTHREADS, 1)
     for (int t = 0; t < nmma; ++t) {
       long long t0 = clk64();
       if ((used >> w) & 1u) {
-        mbar_wait(s_free + w, (c_s >> w) & 1u);
+        bwait(s_free + w, (c_s >> w) & 1u, p.xflags & 2);
         c_s ^= 1u << w;
       }
       used |= 1u << w;
       long long t1 = clk64();
-      mbar_wait(k_full + ks, (kph >> ks) & 1u);
+      bwait(k_full + ks, (kph >> ks) & 1u, p.xflags & 2);
       kph ^= 1u << ks;
       long long t2 = clk64();
       IA_TADD(8, t1 - t0);
@@ -355,9 +361,9 @@ __global__ void __launch_bounds__(Cfg<DP>::NTHREADS, 1)
     for (int n = 0; n < n_kt_b; ++n) {
       const int pb = w * C::NPB + tl % C::NPB;
       long long t0 = clk64();
-      mbar_wait(p_full + pb, (uint32_t)(tl / C::NPB) & 1u);
+      bwait(p_full + pb, (uint32_t)(tl / C::NPB) & 1u, p.xflags & 8);
       long long t1 = clk64();
-      mbar_wait(v_full + vs, vph);
+      bwait(v_full + vs, vph, p.xflags & 8);
       long long t2 = clk64();
       IA_TADD(11, t1 - t0);
       IA_TADD(12, t2 - t1);
@@ -397,15 +403,15 @@ __global__ void __launch_bounds__(Cfg<DP>::NTHREADS, 1)
     // flight per wait); S[w] is handed back to the MMA warp right after the last
     // load of the tile, in every pass.
     const bool tm = (threadIdx.x == 128);
-    const bool trw = IA_PROFILE && ((threadIdx.x & 127) == 0);
+    const bool trw = IA_PROFILE && lane == 0;  // one trace segment per softmax warp
     if (tm) IA_TMARK(0);
     // ---- pass 1: row max over unmasked keys (softmax.py:139-143, :174-179); the row
     // min rides along (free: pass 1 waits on the MMA) to size the unclipped index range
     int32_t mx = INT_MIN, mn = INT_MAX;
     for (int n = wg; n < n_kt; n += NWG) {
       long long tw0 = clk64();
-      mbar_wait(s_full + wg, s_ph);
-      if (trw) IA_TRACE(4 + wg, 8, 0 * n_kt + n);
+      bwait(s_full + wg, s_ph, p.xflags & 4);
+      if (trw) IA_TRACE(warp, 8, 0 * n_kt + n);
       s_ph ^= 1u;
       if (tm) IA_TADD(15, clk64() - tw0);
       tc_fence_after();
@@ -416,7 +422,7 @@ __global__ void __launch_bounds__(Cfg<DP>::NTHREADS, 1)
         if (hb == BN / 64 - 1 && !resident) {
           tc_fence_before();
           mbar_arrive(s_free + wg);
-          if (trw) IA_TRACE(4 + wg, 9, 0 * n_kt + n);
+          if (trw) IA_TRACE(warp, 9, 0 * n_kt + n);
         }
         const int j0 = n * BN + hb * 64;
         if (DEBUG && p.dbg_logits && i < p.L) {
@@ -491,8 +497,8 @@ __global__ void __launch_bounds__(Cfg<DP>::NTHREADS, 1)
     for (int n = wg; n < n_kt_b; n += NWG) {
       if (!resident) {
         long long tw0 = clk64();
-        mbar_wait(s_full + wg, s_ph);
-        if (trw) IA_TRACE(4 + wg, 8, 1 * n_kt + n);
+        bwait(s_full + wg, s_ph, p.xflags & 4);
+        if (trw) IA_TRACE(warp, 8, 1 * n_kt + n);
         s_ph ^= 1u;
         if (tm) IA_TADD(14, clk64() - tw0);
       }
@@ -504,7 +510,7 @@ __global__ void __launch_bounds__(Cfg<DP>::NTHREADS, 1)
         if (hb == BN / 64 - 1 && !resident) {
           tc_fence_before();
           mbar_arrive(s_free + wg);
-          if (trw) IA_TRACE(4 + wg, 9, 1 * n_kt + n);
+          if (trw) IA_TRACE(warp, 9, 1 * n_kt + n);
         }
         if (SKEL) continue;
         const int j0 = n * BN + hb * 64;
@@ -570,8 +576,8 @@ __global__ void __launch_bounds__(Cfg<DP>::NTHREADS, 1)
     for (int n = wg; n < n_kt_b; n += NWG) {
       if (!resident) {
         long long tw0 = clk64();
-        mbar_wait(s_full + wg, s_ph);
-        if (trw) IA_TRACE(4 + wg, 8, 2 * n_kt + n);
+        bwait(s_full + wg, s_ph, p.xflags & 4);
+        if (trw) IA_TRACE(warp, 8, 2 * n_kt + n);
         s_ph ^= 1u;
         if (tm) IA_TADD(14, clk64() - tw0);
       }
@@ -581,7 +587,7 @@ __global__ void __launch_bounds__(Cfg<DP>::NTHREADS, 1)
       // the P.V that last read this P^ buffer must be done (first use passes at once)
       long long tq0 = clk64();
       mbar_wait(p_free + wg * C::NPB + pbl, ((uint32_t)(tl / C::NPB) & 1u) ^ 1u);
-      if (trw) IA_TRACE(4 + wg, 10, 2 * n_kt + n);
+      if (trw) IA_TRACE(warp, 10, 2 * n_kt + n);
       if (tm) IA_TADD(13, clk64() - tq0);
 #pragma unroll 1
       for (int hb = 0; hb < BN / 64; ++hb) {
@@ -590,7 +596,7 @@ __global__ void __launch_bounds__(Cfg<DP>::NTHREADS, 1)
         if (hb == BN / 64 - 1 && !resident) {
           tc_fence_before();
           mbar_arrive(s_free + wg);
-          if (trw) IA_TRACE(4 + wg, 9, 2 * n_kt + n);
+          if (trw) IA_TRACE(warp, 9, 2 * n_kt + n);
         }
         const int j0 = n * BN + hb * 64;
         uint32_t pk[16];
@@ -608,6 +614,16 @@ __global__ void __launch_bounds__(Cfg<DP>::NTHREADS, 1)
               const uint32_t p1 = lds_u32(tab_row + (im.idx_u((int32_t)v4[1]) << 9));
               const uint32_t p2 = lds_u32(tab_row + (im.idx_u((int32_t)v4[2]) << 9));
               const uint32_t p3 = lds_u32(tab_row + (im.idx_u((int32_t)v4[3]) << 9));
+              pk[q] = __byte_perm(__byte_perm(p0, p1, 0x0040), __byte_perm(p2, p3, 0x0040), 0x5410);
+            }
+          } else if (!any_cut) {
+#pragma unroll
+            for (int q = 0; q < 16; ++q) {
+              const uint32_t* v4 = q < 8 ? &va[4 * q] : &vb[4 * (q - 8)];
+              const uint32_t p0 = lds_u32(tab_row + (im.idx_s((int32_t)v4[0]) << 9));
+              const uint32_t p1 = lds_u32(tab_row + (im.idx_s((int32_t)v4[1]) << 9));
+              const uint32_t p2 = lds_u32(tab_row + (im.idx_s((int32_t)v4[2]) << 9));
+              const uint32_t p3 = lds_u32(tab_row + (im.idx_s((int32_t)v4[3]) << 9));
               pk[q] = __byte_perm(__byte_perm(p0, p1, 0x0040), __byte_perm(p2, p3, 0x0040), 0x5410);
             }
           } else {
@@ -655,7 +671,7 @@ __global__ void __launch_bounds__(Cfg<DP>::NTHREADS, 1)
       }
       fence_proxy_async_smem();
       mbar_arrive(p_full + wg * C::NPB + pbl);
-      if (trw) IA_TRACE(4 + wg, 11, 2 * n_kt + n);
+      if (trw) IA_TRACE(warp, 11, 2 * n_kt + n);
       ++tl;
     }
 

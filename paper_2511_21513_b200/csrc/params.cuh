@@ -114,6 +114,7 @@ struct IdxMap {
   uint32_t shift;
   __device__ __forceinline__ void init(int32_t m, const ia_head_params& hp, uint32_t k) {
     nk2 = 0u - 2u * k;
+    asm("" : "+r"(nk2));  // keep -2k in a register (a uniform one is re-negated per use)
     magic = hp.magic;
     mul2 = hp.use32 ? (1u << (32 - hp.shift)) : 0u;
     shift = (uint32_t)hp.shift;

@@ -17,13 +17,13 @@ lut = E.lut_bytes(5, 6.6)
 prep = E.prepare(q, k, v, seq_lens=sl, scale_granularity=wl.scale_granularity)
 out = torch.empty_like(q)
 grid = ((L + 127) // 128) * B * H
-times = torch.zeros(grid * 16 + 14 * 2048, dtype=torch.int64, device=dev)
+times = torch.zeros(grid * 16 + 32 * 2048, dtype=torch.int64, device=dev)
 for it in range(3):
     times.zero_()
     E.attn_fused(prep, (B, H, Hkv, L, d), out, causal=wl.causal, seq_lens=sl, lut=lut, times=times)
 torch.cuda.synchronize()
 t = times.cpu().numpy()
-tr = t[grid * 16:].reshape(2, 7, 2048)
+tr = t[grid * 16:].reshape(2, 16, 2048)
 os.makedirs("gpurun_out", exist_ok=True)
 np.savez(f"gpurun_out/trace_{name}.npz", tr=tr, slots=t[:grid * 16].reshape(grid, 16))
 NAMES = {1: "Kprod got k_empty", 2: "QK got s_free", 3: "QK got k_full", 4: "QK committed",
@@ -34,7 +34,7 @@ for c in range(2):
     allc = seg[seg != 0] >> 16
     t0 = allc.min()
     print(f"== CTA {'0' if c == 0 else 1000}: span {allc.max() - t0} cycles")
-    for s in range(7):
+    for s in range(16):
         e = seg[s][seg[s] != 0]
         if len(e) == 0:
             continue
