@@ -211,6 +211,11 @@ __global__ void __launch_bounds__(Cfg<DP>::NTHREADS, 1)
   const int q0 = qt * BM;
   const int len = p.seq_lens ? min(p.seq_lens[b], p.L) : p.L;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  // Softmax warpgroups are warps 0 .. 4*NWG-1; the four role warps come last.  The
+  // warp scheduler favours the highest warp id among eligible warps, so the
+  // latency-critical TMA / MMA issue loops win their issue slots over the
+  // arithmetic-heavy softmax warps sharing their SM sub-partition.
+  const int rw = warp - 4 * NWG;  // role: 0 K producer, 1 QK^T, 2 V^T producer + TMEM alloc, 3 P.V
 
   if (q0 >= len) {  // the whole query tile is padding: +0.0 rows (pipeline contract)
     const int rows = min(BM, p.L - q0);
@@ -218,14 +223,14 @@ __global__ void __launch_bounds__(Cfg<DP>::NTHREADS, 1)
     for (int t = threadIdx.x; t < rows * p.d; t += C::NTHREADS) o[t] = 0.0f;
     return;
   }
-  if (threadIdx.x == 0) IA_TMARK(6);
+  if (threadIdx.x == 128 * NWG) IA_TMARK(6);
   const int key_end = p.causal ? min(q0 + BM, len) : len;
   const int n_kt = (key_end + BN - 1) / BN;
   const bool resident = n_kt <= NWG;  // every logit tile fits its own TMEM buffer
   const int npass = resident ? 1 : ((p.xflags & 1) ? 1 : 3);
   const int n_kt_b = (p.xflags & 1) ? 0 : n_kt;  // key tiles of passes 2-3 / P.V
 
-  if (warp == 0 && lane == 0) {
+  if (rw == 0 && lane == 0) {
     prefetch_tmap(&tmq);
     prefetch_tmap(&tmk);
     prefetch_tmap(&tmv);
@@ -234,16 +239,16 @@ __global__ void __launch_bounds__(Cfg<DP>::NTHREADS, 1)
     for (int s = 0; s < C::NVST; ++s) { mbar_init(v_full + s, 1); mbar_init(v_empty + s, 1); }
     for (int w = 0; w < NWG; ++w) {
       mbar_init(s_full + w, 1);
-      mbar_init(s_free + w, 128);
+      mbar_init(s_free + w, 4);  // one arrive per warp of the warpgroup
     }
     for (int w = 0; w < NWG * C::NPB; ++w) {
-      mbar_init(p_full + w, 128);
+      mbar_init(p_full + w, 4);
       mbar_init(p_free + w, 1);
     }
     mbar_init(o_full, 1);
     fence_mbar_init();
   }
-  if (warp == 2) {
+  if (rw == 2) {
     tmem_alloc(tmem_slot, TMEM_COLS);
     tmem_relinquish();
   }
@@ -265,7 +270,7 @@ __global__ void __launch_bounds__(Cfg<DP>::NTHREADS, 1)
   // measured to cost ~1000 cycles per tile.  Keeping the two MMA streams in
   // separate warps lets QK^T(n + NWG) start as soon as S[w] is read back,
   // independent of P.V(n) progress.
-  if (warp == 0) {
+  if (rw == 0) {
     // ------------------------------------------------------------ K producer (+ Q)
     if (elect_one()) {
       mbar_expect_tx(q_full, C::Q_BYTES);
@@ -293,7 +298,7 @@ __global__ void __launch_bounds__(Cfg<DP>::NTHREADS, 1)
       if (t + 1 < t3 ? ks == C::NKX : ks == C::NKST) ks = 0;
       if (t + 1 == t3) ks = 0;
     }
-  } else if (warp == 2) {
+  } else if (rw == 2) {
     // ------------------------------------------------------------ V^T producer
     int vs = 0, vph = 0;
     for (int n = 0; n < n_kt_b; ++n) {
@@ -306,7 +311,7 @@ __global__ void __launch_bounds__(Cfg<DP>::NTHREADS, 1)
       __syncwarp();
       if (++vs == C::NVST) { vs = 0; vph ^= 1; }
     }
-  } else if (warp == 1) {
+  } else if (rw == 1) {
     // ------------------------------------------------------------ QK^T issuer
     // Tile n of every pass lives in TMEM buffer / warpgroup w = n % NWG.
     constexpr uint32_t idq = idesc_i8(BM, BN, true, true);  // s8 x s8 -> s32
@@ -320,11 +325,13 @@ __global__ void __launch_bounds__(Cfg<DP>::NTHREADS, 1)
     const int nmma = npass * n_kt;
     for (int t = 0; t < nmma; ++t) {
       long long t0 = clk64();
+      if (lane == 0) IA_TRACE(1, 2, t);
       if ((used >> w) & 1u) {
         bwait(s_free + w, (c_s >> w) & 1u, p.xflags & 2);
         c_s ^= 1u << w;
       }
       used |= 1u << w;
+      if (lane == 0) IA_TRACE(1, 5, t);
       long long t1 = clk64();
       bwait(k_full + ks, (kph >> ks) & 1u, p.xflags & 2);
       kph ^= 1u << ks;
@@ -352,7 +359,7 @@ __global__ void __launch_bounds__(Cfg<DP>::NTHREADS, 1)
       if (t + 1 < t3 ? ks == C::NKX : ks == C::NKST) ks = 0;
       if (t + 1 == t3) ks = 0;
     }
-  } else if (warp == 3) {
+  } else if (rw == 3) {
     // ------------------------------------------------------------ P.V issuer
     constexpr uint32_t idv = idesc_i8(BM, DP, false, true);  // u8 x s8 -> s32
     const uint64_t dp0 = sdesc(smem_u32(smem + C::OFF_P), 1024, 2u);
@@ -384,9 +391,9 @@ __global__ void __launch_bounds__(Cfg<DP>::NTHREADS, 1)
     }
     if (elect_one()) tc_commit(o_full);
     __syncwarp();
-  } else if (warp >= 4) {
+  } else if (rw < 0) {
     // ------------------------------------------------------------ IndexSoftmax warpgroups
-    const int wg = (warp - 4) >> 2;
+    const int wg = warp >> 2;
     const int quad = warp & 3;  // TMEM lane quadrant accessible to this warp
     const int row = quad * 32 + lane;
     const int i = q0 + row;
@@ -402,7 +409,7 @@ __global__ void __launch_bounds__(Cfg<DP>::NTHREADS, 1)
     // Each tile is read from TMEM in two 64-column batches (two x32 loads in
     // flight per wait); S[w] is handed back to the MMA warp right after the last
     // load of the tile, in every pass.
-    const bool tm = (threadIdx.x == 128);
+    const bool tm = (threadIdx.x == 0);
     const bool trw = IA_PROFILE && lane == 0;  // one trace segment per softmax warp
     if (tm) IA_TMARK(0);
     // ---- pass 1: row max over unmasked keys (softmax.py:139-143, :174-179); the row
@@ -411,7 +418,7 @@ __global__ void __launch_bounds__(Cfg<DP>::NTHREADS, 1)
     for (int n = wg; n < n_kt; n += NWG) {
       long long tw0 = clk64();
       bwait(s_full + wg, s_ph, p.xflags & 4);
-      if (trw) IA_TRACE(warp, 8, 0 * n_kt + n);
+      if (trw) IA_TRACE(4 + warp, 8, 0 * n_kt + n);
       s_ph ^= 1u;
       if (tm) IA_TADD(15, clk64() - tw0);
       tc_fence_after();
@@ -421,8 +428,9 @@ __global__ void __launch_bounds__(Cfg<DP>::NTHREADS, 1)
         tmem_ld64(s_base + hb * 64, va, vb);
         if (hb == BN / 64 - 1 && !resident) {
           tc_fence_before();
-          mbar_arrive(s_free + wg);
-          if (trw) IA_TRACE(warp, 9, 0 * n_kt + n);
+          __syncwarp();
+          if (lane == 0) mbar_arrive(s_free + wg);
+          if (trw) IA_TRACE(4 + warp, 9, 0 * n_kt + n);
         }
         const int j0 = n * BN + hb * 64;
         if (DEBUG && p.dbg_logits && i < p.L) {
@@ -498,7 +506,7 @@ __global__ void __launch_bounds__(Cfg<DP>::NTHREADS, 1)
       if (!resident) {
         long long tw0 = clk64();
         bwait(s_full + wg, s_ph, p.xflags & 4);
-        if (trw) IA_TRACE(warp, 8, 1 * n_kt + n);
+        if (trw) IA_TRACE(4 + warp, 8, 1 * n_kt + n);
         s_ph ^= 1u;
         if (tm) IA_TADD(14, clk64() - tw0);
       }
@@ -509,8 +517,9 @@ __global__ void __launch_bounds__(Cfg<DP>::NTHREADS, 1)
         tmem_ld64(s_base + hb * 64, va, vb);
         if (hb == BN / 64 - 1 && !resident) {
           tc_fence_before();
-          mbar_arrive(s_free + wg);
-          if (trw) IA_TRACE(warp, 9, 1 * n_kt + n);
+          __syncwarp();
+          if (lane == 0) mbar_arrive(s_free + wg);
+          if (trw) IA_TRACE(4 + warp, 9, 1 * n_kt + n);
         }
         if (SKEL) continue;
         const int j0 = n * BN + hb * 64;
@@ -577,7 +586,7 @@ __global__ void __launch_bounds__(Cfg<DP>::NTHREADS, 1)
       if (!resident) {
         long long tw0 = clk64();
         bwait(s_full + wg, s_ph, p.xflags & 4);
-        if (trw) IA_TRACE(warp, 8, 2 * n_kt + n);
+        if (trw) IA_TRACE(4 + warp, 8, 2 * n_kt + n);
         s_ph ^= 1u;
         if (tm) IA_TADD(14, clk64() - tw0);
       }
@@ -587,7 +596,7 @@ __global__ void __launch_bounds__(Cfg<DP>::NTHREADS, 1)
       // the P.V that last read this P^ buffer must be done (first use passes at once)
       long long tq0 = clk64();
       mbar_wait(p_free + wg * C::NPB + pbl, ((uint32_t)(tl / C::NPB) & 1u) ^ 1u);
-      if (trw) IA_TRACE(warp, 10, 2 * n_kt + n);
+      if (trw) IA_TRACE(4 + warp, 10, 2 * n_kt + n);
       if (tm) IA_TADD(13, clk64() - tq0);
 #pragma unroll 1
       for (int hb = 0; hb < BN / 64; ++hb) {
@@ -595,8 +604,9 @@ __global__ void __launch_bounds__(Cfg<DP>::NTHREADS, 1)
         tmem_ld64(s_base + hb * 64, va, vb);
         if (hb == BN / 64 - 1 && !resident) {
           tc_fence_before();
-          mbar_arrive(s_free + wg);
-          if (trw) IA_TRACE(warp, 9, 2 * n_kt + n);
+          __syncwarp();
+          if (lane == 0) mbar_arrive(s_free + wg);
+          if (trw) IA_TRACE(4 + warp, 9, 2 * n_kt + n);
         }
         const int j0 = n * BN + hb * 64;
         uint32_t pk[16];
@@ -670,8 +680,9 @@ __global__ void __launch_bounds__(Cfg<DP>::NTHREADS, 1)
         }
       }
       fence_proxy_async_smem();
-      mbar_arrive(p_full + wg * C::NPB + pbl);
-      if (trw) IA_TRACE(warp, 11, 2 * n_kt + n);
+      __syncwarp();
+      if (lane == 0) mbar_arrive(p_full + wg * C::NPB + pbl);
+      if (trw) IA_TRACE(4 + warp, 11, 2 * n_kt + n);
       ++tl;
     }
 
@@ -700,7 +711,7 @@ __global__ void __launch_bounds__(Cfg<DP>::NTHREADS, 1)
     named_bar_sync(1, NWT);
     const int rows = min(BM, p.L - q0);
     float* obase = p.out + ((size_t)bh * p.L + q0) * p.d;
-    const int tid = threadIdx.x - 128;
+    const int tid = threadIdx.x;
     if ((p.d & 3) == 0) {
       const int d4 = p.d >> 2;
       for (int t = tid; t < rows * d4; t += NWT) {
@@ -723,8 +734,8 @@ __global__ void __launch_bounds__(Cfg<DP>::NTHREADS, 1)
   }
   tc_fence_before();
   __syncthreads();
-  if (threadIdx.x == 0) { IA_TMARK(5); if (IA_PROFILE && p.dbg_times) p.dbg_times[(size_t)blockIdx.x * 16 + 10] = n_kt; }
-  if (warp == 2) {
+  if (threadIdx.x == 128 * NWG) { IA_TMARK(5); if (IA_PROFILE && p.dbg_times) p.dbg_times[(size_t)blockIdx.x * 16 + 10] = n_kt; }
+  if (rw == 2) {
     tc_fence_after();
     tmem_dealloc(tmem, TMEM_COLS);
   }
