@@ -270,7 +270,9 @@ def attention(q, k, v, *, causal=False, seq_lens=None, mask=None, scale_granular
                mask_bits=mbits, lut=lut, p_scale=p_scale, debug=dbg)
     if timer is not None:
         timer.mark("attention")
-    if check_finite:
+    if isinstance(check_finite, list):  # deferred: the caller checks after its pipeline
+        check_finite.append(prep.err)
+    elif check_finite:
         raise_if_nonfinite(prep.err)
     if debug:
         dbg.update(qhat=prep.qhat, khat=prep.khat, vt=prep.vt, q_scales=prep.q_scales,
@@ -337,7 +339,9 @@ def _attention_unfused(q, k, v, *, causal, seq_lens, mask, scale_granularity, b,
                   slot_div=1 if per_head else B * Hkv)
     quantize_vt(v, B * Hkv, Lq, d, sv, vt, lp, dp * lp, seq_lens=seq_lens, valid_div=Hkv,
                 slot_div=1 if per_head else B * Hkv)
-    if check_finite:
+    if isinstance(check_finite, list):
+        check_finite.append(ws.err)
+    elif check_finite:
         raise_if_nonfinite(ws.err)
     sq_h, sk_h, sv_h = sq.cpu().numpy(), sk.cpu().numpy(), sv.cpu().numpy()
     lens = None if seq_lens is None else seq_lens.cpu().numpy()
