@@ -326,14 +326,16 @@ __global__ void __launch_bounds__(Cfg<DP>::NTHREADS, 1)
     for (int t = 0; t < nmma; ++t) {
       long long t0 = clk64();
       if (lane == 0) IA_TRACE(1, 2, t);
-      if ((used >> w) & 1u) {
-        bwait(s_free + w, (c_s >> w) & 1u, p.xflags & 2);
-        c_s ^= 1u << w;
-      }
+      // both readiness tests in flight at once; block only on what is not ready yet
+      const bool need_free = (used >> w) & 1u;
+      const uint32_t f_ok = need_free ? mbar_test(s_free + w, (c_s >> w) & 1u) : 1u;
+      const uint32_t k_ok = mbar_test(k_full + ks, (kph >> ks) & 1u);
+      if (!f_ok) bwait(s_free + w, (c_s >> w) & 1u, p.xflags & 2);
+      if (need_free) c_s ^= 1u << w;
       used |= 1u << w;
       if (lane == 0) IA_TRACE(1, 5, t);
       long long t1 = clk64();
-      bwait(k_full + ks, (kph >> ks) & 1u, p.xflags & 2);
+      if (!k_ok) bwait(k_full + ks, (kph >> ks) & 1u, p.xflags & 2);
       kph ^= 1u << ks;
       long long t2 = clk64();
       IA_TADD(8, t1 - t0);

@@ -78,6 +78,19 @@ __device__ __forceinline__ uint32_t mbar_poll(uint32_t bar, uint32_t parity) {
       : "memory");
   return ok;
 }
+// Non-blocking phase test (mbarrier.test_wait): lets a thread put several barrier
+// checks in flight before it consumes any of the results.
+__device__ __forceinline__ uint32_t mbar_test(uint64_t* bar, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "mbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+      "selp.u32 %0, 1, 0, p;\n\t}"
+      : "=r"(ok)
+      : "r"(smem_u32(bar)), "r"(parity)
+      : "memory");
+  return ok;
+}
 __device__ __forceinline__ void mbar_wait_spin(uint64_t* bar, uint32_t parity) {
   const uint32_t a = smem_u32(bar);
   uint32_t spins = 0;
