@@ -94,6 +94,7 @@ typedef struct ia_head_params {
   float out_scale;
   float s_q, s_k, s_v;
   int32_t unc32;    /* 1: the magic is also exact without the clip (n up to 2k*2*d*127^2 + c_eff) */
+  uint32_t magic9;  /* 0, or: idx * 512 = umulhi(n, magic9) & ~511 for the clipped n range */
 } ia_head_params;
 
 int ia_head_params_host(double c, int64_t d, int nlut, int p_scale, float s_q, float s_k,

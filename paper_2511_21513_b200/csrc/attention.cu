@@ -577,6 +577,8 @@ __global__ void __launch_bounds__(Cfg<DP>::NTHREADS, 1)
     // entry idx of this row: wide: tab_row + idx * 512 (u32), else tab_row + idx * 128 (u8)
     const uint32_t tab_row = smem_u32(tab) + (uint32_t)row * (wtab ? 4u : 1u);
     const uint32_t tab_sh = wtab ? 9u : 7u;
+    const uint32_t tab0 = smem_u32(tab), row4 = (uint32_t)row * 4u;
+    const uint32_t m9 = (wtab && !(p.xflags & 256)) ? hp.magic9 : 0u;
     // this thread's row of its warpgroup's P^ tile (K-major, 128B swizzle: 16-byte
     // unit x of row r lives at unit x ^ (r % 8))
     const uint32_t p_rows = smem_u32(smem + C::OFF_P + wg * C::NPB * C::P_BYTES) + (uint32_t)row * 128;
@@ -626,6 +628,17 @@ __global__ void __launch_bounds__(Cfg<DP>::NTHREADS, 1)
               const uint32_t p1 = lds_u32(tab_row + (im.idx_u((int32_t)v4[1]) << 9));
               const uint32_t p2 = lds_u32(tab_row + (im.idx_u((int32_t)v4[2]) << 9));
               const uint32_t p3 = lds_u32(tab_row + (im.idx_u((int32_t)v4[3]) << 9));
+              pk[q] = __byte_perm(__byte_perm(p0, p1, 0x0040), __byte_perm(p2, p3, 0x0040), 0x5410);
+            }
+          } else if (!any_cut && m9) {
+            // address = (umulhi(n, magic9) & ~511) | row*4: no shift, no address IMAD
+#pragma unroll
+            for (int q = 0; q < 16; ++q) {
+              const uint32_t* v4 = q < 8 ? &va[4 * q] : &vb[4 * (q - 8)];
+              const uint32_t p0 = lds_u32(tab0 + ((__umulhi(im.n_clip((int32_t)v4[0]), m9) & 0xFFFFFE00u) | row4));
+              const uint32_t p1 = lds_u32(tab0 + ((__umulhi(im.n_clip((int32_t)v4[1]), m9) & 0xFFFFFE00u) | row4));
+              const uint32_t p2 = lds_u32(tab0 + ((__umulhi(im.n_clip((int32_t)v4[2]), m9) & 0xFFFFFE00u) | row4));
+              const uint32_t p3 = lds_u32(tab0 + ((__umulhi(im.n_clip((int32_t)v4[3]), m9) & 0xFFFFFE00u) | row4));
               pk[q] = __byte_perm(__byte_perm(p0, p1, 0x0040), __byte_perm(p2, p3, 0x0040), 0x5410);
             }
           } else if (!any_cut) {

@@ -85,6 +85,24 @@ __host__ __device__ inline void fill_head_params(int64_t c_int, int64_t dbound, 
     }
   }
   if (!hp->use32) hp->unc32 = 0;
+  // Scaled magic for the clipped range n <= (2k+1) c_eff: with M9 the magic of shift
+  // s9 <= 9 and magic9 = M9 << (9 - s9), umulhi(n, magic9) = idx * 512 + r with
+  // r < 512 (floor(floor(x * 2^j) / 2^j) = floor(x)), so a row-table address
+  // idx * 512 + row * 4 is one LOP3 away.  0 when it does not fit 32 bits.
+  hp->magic9 = 0;
+  if (hp->use32) {
+    const int64_t nmc = (2 * k + 1) * c_eff;
+    if (nmc < (int64_t(1) << 31)) {
+      const uint64_t D = 2 * (uint64_t)c_eff;
+      int s9 = bitlen_u64((uint64_t)nmc * D - 1) - 32;
+      if (s9 < 1) s9 = 1;
+      if (s9 <= 9) {
+        const uint64_t M9 = ((uint64_t(1) << (32 + s9)) + D - 1) / D;
+        const uint64_t m9 = M9 << (9 - s9);
+        if (m9 < (uint64_t(1) << 32)) hp->magic9 = (uint32_t)m9;
+      }
+    }
+  }
 }
 
 __host__ __device__ inline void make_head_params(double c, int64_t d, int nlut, int p_scale,
@@ -132,6 +150,10 @@ struct IdxMap {
     const int32_t ac = max(a, lo);
     const uint32_t n = base + nk2 * (uint32_t)ac;
     return __umulhi(n, magic) >> shift;
+  }
+  // n for the clipped delta (the operand of magic9)
+  __device__ __forceinline__ uint32_t n_clip(int32_t a) const {
+    return base + nk2 * (uint32_t)max(a, lo);
   }
   // Unclamped (hp.unc32): floor((2k*delta + c_eff) / (2 c_eff)) for any reachable
   // delta; may exceed k, callers index a table zero-extended past k.

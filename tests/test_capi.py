@@ -78,6 +78,10 @@ def _check_map(hp, k, deltas):
         got_mul = (q * np.uint64(1 << (32 - hp.shift))) >> np.uint64(32)
         assert np.array_equal(got_shf, want)
         assert np.array_equal(got_mul, want)
+    if hp.magic9:  # pass-3 row-table address form: umulhi(n, magic9) & ~511 == idx * 512
+        assert hp.use32 and int(n.max()) <= (2 * k + 1) * c_eff
+        q9 = (n * np.uint64(hp.magic9)) >> np.uint64(32)
+        assert np.array_equal(q9 & np.uint64(0xFFFFFE00), want * np.uint64(512))
 
 
 @pytest.mark.parametrize("b", [2, 5, 8])

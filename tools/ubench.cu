@@ -18,12 +18,13 @@ __device__ __forceinline__ uint64_t clk() {
 // results[0..] : cycles
 __global__ void __launch_bounds__(256, 1) ubench_kernel(uint64_t* res, int iters) {
   extern __shared__ __align__(1024) uint8_t smem[];
-  __shared__ uint64_t bar[4];
+  __shared__ uint64_t bar[8];
   __shared__ uint32_t tslot;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
     for (int i = 0; i < 3; ++i) mbar_init(bar + i, 1);
     mbar_init(bar + 3, 3);
+    for (int i = 4; i < 8; ++i) mbar_init(bar + i, 1);
     fence_mbar_init();
   }
   for (int i = threadIdx.x; i < 32768 / 4; i += 256) reinterpret_cast<uint32_t*>(smem)[i] = i * 2654435761u;
@@ -86,6 +87,47 @@ __global__ void __launch_bounds__(256, 1) ubench_kernel(uint64_t* res, int iters
     res[10] = clk() - t0;
     mbar_wait(bar + 0, ph);
     ph ^= 1;
+  }
+  __syncthreads();
+  // (a3) issue rate of the fused kernel's QK^T step: 24 tiles of {4 MMA (N=128) into a
+  // rotating 128-column buffer + 2 commits}, no waits; then completion
+  if (warp == 1 && lane == 0) {
+    uint64_t da[4], db[4];
+    for (int kk = 0; kk < 4; ++kk) { da[kk] = sdesc(sa + kk * 32, 1024, 2); db[kk] = sdesc(sb + kk * 32, 1024, 2); }
+    uint64_t t0 = clk(), t3 = 0;
+    for (int t = 0; t < 24; ++t) {
+      for (int kk = 0; kk < 4; ++kk) mma_i8_ss(tmem + (t % 3) * 128, da[kk], db[kk], idq, kk > 0);
+      tc_commit(bar + 4);
+      tc_commit(bar + 5);
+      if (t == 2) t3 = clk();
+    }
+    uint64_t t1 = clk();
+    tc_commit(bar + 6);
+    mbar_wait(bar + 6, 0);
+    uint64_t t2 = clk();
+    res[16] = t1 - t0;  // issue time, 24 tiles
+    res[17] = t3 - t0;  // first 3 tiles
+    res[18] = t2 - t0;  // to completion
+    // same with 1 commit per tile
+    t0 = clk();
+    for (int t = 0; t < 24; ++t) {
+      for (int kk = 0; kk < 4; ++kk) mma_i8_ss(tmem + (t % 3) * 128, da[kk], db[kk], idq, kk > 0);
+      tc_commit(bar + 4);
+    }
+    t1 = clk();
+    tc_commit(bar + 6);
+    mbar_wait(bar + 6, 1);
+    res[19] = t1 - t0;
+    res[20] = clk() - t0;
+    // no commits inside
+    t0 = clk();
+    for (int t = 0; t < 24; ++t)
+      for (int kk = 0; kk < 4; ++kk) mma_i8_ss(tmem + (t % 3) * 128, da[kk], db[kk], idq, kk > 0);
+    t1 = clk();
+    tc_commit(bar + 6);
+    mbar_wait(bar + 6, 0);
+    res[21] = t1 - t0;
+    res[22] = clk() - t0;
   }
   __syncthreads();
   // (a2) 3 warps issuing N=64 MMAs concurrently (32 tiles each) into disjoint TMEM
@@ -154,12 +196,12 @@ __global__ void __launch_bounds__(256, 1) ubench_kernel(uint64_t* res, int iters
 
 int main() {
   uint64_t* d;
-  cudaMalloc(&d, 16 * sizeof(uint64_t));
-  cudaMemset(d, 0, 16 * sizeof(uint64_t));
+  cudaMalloc(&d, 32 * sizeof(uint64_t));
+  cudaMemset(d, 0, 32 * sizeof(uint64_t));
   cudaFuncSetAttribute(ubench_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 40000);
   ubench_kernel<<<1, 256, 40000>>>(d, 64);
   cudaError_t e = cudaDeviceSynchronize();
-  uint64_t h[16] = {0};
+  uint64_t h[32] = {0};
   cudaMemcpy(h, d, sizeof(h), cudaMemcpyDeviceToHost);
   printf("status %s\n", cudaGetErrorString(e));
   printf("MMA 128x128x128 i8 issue->commit wait: best %llu avg %llu cycles\n", (unsigned long long)h[0],
@@ -175,5 +217,11 @@ int main() {
          (unsigned long long)h[9], (unsigned long long)h[10]);
   printf("3 warps x 32 N=64 tiles concurrently: issue %llu %llu %llu cycles (%.1f/tile each)\n",
          (unsigned long long)h[11], (unsigned long long)h[12], (unsigned long long)h[13], h[11] / 32.0);
+  printf("24 tiles {4 MMA + 2 commits}: issue %llu (%.1f/tile; first 3 tiles %llu), to completion %llu (%.1f/tile)\n",
+         (unsigned long long)h[16], h[16] / 24.0, (unsigned long long)h[17], (unsigned long long)h[18], h[18] / 24.0);
+  printf("24 tiles {4 MMA + 1 commit}: issue %llu (%.1f/tile), completion %llu\n", (unsigned long long)h[19],
+         h[19] / 24.0, (unsigned long long)h[20]);
+  printf("24 tiles {4 MMA}: issue %llu (%.1f/tile), completion %llu\n", (unsigned long long)h[21], h[21] / 24.0,
+         (unsigned long long)h[22]);
   return 0;
 }
