@@ -54,14 +54,19 @@ __device__ __forceinline__ uint32_t mbar_try_wait(uint32_t bar, uint32_t parity)
   return ok;
 }
 
-// Wait for the phase with the given parity to complete.  A watchdog traps
-// after ~8000 suspend windows so a protocol bug surfaces as a launch error
-// instead of a hung GPU.
+// Wait for the phase with the given parity to complete.  A watchdog traps after
+// ~2^40 SM cycles (~9 min) so a protocol bug surfaces as a launch error instead of
+// a hung GPU.  It is time-based: a suspended try_wait returns on any barrier event
+// of the CTA, so a spin count says nothing about elapsed time (a role that idles
+// through whole passes, or a kernel slowed down by a profiler's replay, would trip
+// a count-based limit).
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   const uint32_t a = smem_u32(bar);
+  if (mbar_try_wait(a, parity)) return;
+  const long long t0 = clock64();
   uint32_t spins = 0;
   while (!mbar_try_wait(a, parity)) {
-    if (++spins > (IA_WAIT_HINT_NS > 0 ? 8000u : 400000000u)) __trap();
+    if ((++spins & 1023u) == 0 && clock64() - t0 > (1ll << 40)) __trap();
   }
 }
 
@@ -93,9 +98,10 @@ __device__ __forceinline__ uint32_t mbar_test(uint64_t* bar, uint32_t parity) {
 }
 __device__ __forceinline__ void mbar_wait_spin(uint64_t* bar, uint32_t parity) {
   const uint32_t a = smem_u32(bar);
+  const long long t0 = clock64();
   uint32_t spins = 0;
   while (!mbar_poll(a, parity)) {
-    if (++spins > 400000000u) __trap();
+    if ((++spins & 1023u) == 0 && clock64() - t0 > (1ll << 40)) __trap();
   }
 }
 
