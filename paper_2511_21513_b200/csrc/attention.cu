@@ -172,25 +172,6 @@ __device__ __forceinline__ void bwait(uint64_t* bar, uint32_t parity, bool spin)
   else mbar_wait(bar, parity);
 }
 
-// K stage of QK^T tile t (pass-major, t = pass * n_kt + n) and the parity of its
-// use: passes 1-2 cycle through NKX stages, pass 3 through the NKST regular ones.
-// The MMA's single commit goes to k_empty[stage]; the softmax warpgroup that owns
-// the tile waits on that same phase (the K producer waits on it too before
-// refilling the stage, so the phase cannot run two ahead of either waiter).
-template <class C>
-__device__ __forceinline__ void k_stage_phase(int t, int n_kt, int& ks, uint32_t& ph) {
-  const int t3 = 2 * n_kt;
-  if (t < t3) {
-    ks = t % C::NKX;
-    ph = (uint32_t)(t / C::NKX) & 1u;
-  } else {
-    const int r = t - t3;
-    ks = r % C::NKST;
-    const int u12 = t3 > ks ? (t3 - ks + C::NKX - 1) / C::NKX : 0;
-    ph = (uint32_t)(u12 + r / C::NKST) & 1u;
-  }
-}
-
 template <int DP, bool DEBUG, bool SKEL = false>
 __global__ void __launch_bounds__(Cfg<DP>::NTHREADS, 1)
     attn_fwd_kernel(const __grid_constant__ CUtensorMap tmq,
@@ -215,7 +196,8 @@ __global__ void __launch_bounds__(Cfg<DP>::NTHREADS, 1)
   uint64_t* k_empty = k_full + C::NKX;
   uint64_t* v_full = k_empty + C::NKX;
   uint64_t* v_empty = v_full + C::NVST;
-  uint64_t* s_free = v_empty + C::NVST;    // [NWG] softmax -> QK issuer (S[w] fully read)
+  uint64_t* s_full = v_empty + C::NVST;       // [NWG] QK issuer -> softmax (QK^T landed in S[w])
+  uint64_t* s_free = s_full + NWG;         // [NWG] softmax -> QK issuer (S[w] fully read)
   uint64_t* p_full = s_free + NWG;         // [NWG*NPB] softmax -> P.V issuer (P^ tile in smem)
   uint64_t* p_free = p_full + NWG * C::NPB;  // [NWG*NPB] P.V issuer -> softmax (tile consumed)
   uint64_t* o_full = p_free + NWG * C::NPB;  // P.V issuer -> epilogue
@@ -256,6 +238,7 @@ __global__ void __launch_bounds__(Cfg<DP>::NTHREADS, 1)
     for (int s = 0; s < C::NKX; ++s) { mbar_init(k_full + s, 1); mbar_init(k_empty + s, 1); }
     for (int s = 0; s < C::NVST; ++s) { mbar_init(v_full + s, 1); mbar_init(v_empty + s, 1); }
     for (int w = 0; w < NWG; ++w) {
+      mbar_init(s_full + w, 1);
       mbar_init(s_free + w, 4);  // one arrive per warp of the warpgroup
     }
     for (int w = 0; w < NWG * C::NPB; ++w) {
@@ -367,7 +350,8 @@ __global__ void __launch_bounds__(Cfg<DP>::NTHREADS, 1)
           const uint32_t off = (kk * 32 / C::SW) * C::SUB_BYTES + (kk * 32) % C::SW;
           mma_i8_ss(dt, dq + (off >> 4), dk + (off >> 4), idq, kk > 0);
         }
-        tc_commit(k_empty + ks);  // frees the K stage and tells warpgroup w its S tile landed
+        tc_commit(k_empty + ks);
+        tc_commit(s_full + w);
         IA_TRACE(1, 4, t);
       }
       __syncwarp();
@@ -422,12 +406,7 @@ __global__ void __launch_bounds__(Cfg<DP>::NTHREADS, 1)
     const ia_head_params hp = p.params[bh];
     const uint32_t k = (uint32_t)(nlut - 1);
     constexpr int NWT = 128 * NWG;  // softmax threads
-    auto s_wait = [&](int t) {  // QK^T tile t has landed in S[wg]
-      int ks;
-      uint32_t ph;
-      k_stage_phase<C>(t, n_kt, ks, ph);
-      bwait(k_empty + ks, ph, p.xflags & 4);
-    };
+    uint32_t s_ph = 0;              // phase of s_full[wg]
 
     // Each tile is read from TMEM in two 64-column batches (two x32 loads in
     // flight per wait); S[w] is handed back to the MMA warp right after the last
@@ -440,8 +419,9 @@ __global__ void __launch_bounds__(Cfg<DP>::NTHREADS, 1)
     int32_t mx = INT_MIN, mn = INT_MAX;
     for (int n = wg; n < n_kt; n += NWG) {
       long long tw0 = clk64();
-      s_wait(n);
+      bwait(s_full + wg, s_ph, p.xflags & 4);
       if (trw) IA_TRACE(4 + warp, 8, 0 * n_kt + n);
+      s_ph ^= 1u;
       if (tm) IA_TADD(15, clk64() - tw0);
       tc_fence_after();
 #pragma unroll 1
@@ -527,8 +507,9 @@ __global__ void __launch_bounds__(Cfg<DP>::NTHREADS, 1)
     for (int n = wg; n < n_kt_b; n += NWG) {
       if (!resident) {
         long long tw0 = clk64();
-        s_wait(n_kt + n);
+        bwait(s_full + wg, s_ph, p.xflags & 4);
         if (trw) IA_TRACE(4 + warp, 8, 1 * n_kt + n);
+        s_ph ^= 1u;
         if (tm) IA_TADD(14, clk64() - tw0);
       }
       tc_fence_after();
@@ -608,8 +589,9 @@ __global__ void __launch_bounds__(Cfg<DP>::NTHREADS, 1)
     for (int n = wg; n < n_kt_b; n += NWG) {
       if (!resident) {
         long long tw0 = clk64();
-        s_wait(2 * n_kt + n);
+        bwait(s_full + wg, s_ph, p.xflags & 4);
         if (trw) IA_TRACE(4 + warp, 8, 2 * n_kt + n);
+        s_ph ^= 1u;
         if (tm) IA_TADD(14, clk64() - tw0);
       }
       tc_fence_after();
