@@ -19,7 +19,7 @@
 extern "C" {
 #endif
 
-#define IA_ABI_VERSION 1
+#define IA_ABI_VERSION 2  /* 2: ia_head_params gained magic9 */
 #define IA_MAX_SEQ_LEN 65536   /* gemm.py:26 MAX_SEQ_LEN */
 #define IA_MAX_HEAD_DIM 131070 /* gemm.py:25 MAX_HEAD_DIM */
 #define IA_FUSED_MAX_HEAD_DIM 256
