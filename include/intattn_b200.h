@@ -76,6 +76,20 @@ int ia_quantize(const float* x, int64_t n_rowgroups, int64_t rows_per_group, int
                 const int32_t* valid_rows, int64_t valid_div, int mode, int64_t slot_div,
                 int64_t col_group, const float* scales, int8_t* out, int64_t out_pitch,
                 int transpose, int64_t out_group_stride, void* stream);
+/* Per-head quantisation of Q, K and V in one launch: the three
+ * quantize_symmetric calls of int_attention (pipeline.py:217-219) for every
+ * (batch, head) slab of q [B, H, L, d], k and v [B, Hkv, L, d] (f32,
+ * row-major, 16-byte aligned, d % 4 == 0, d <= 256).  Writes qhat
+ * [B*H, L, d_pad] and khat [B*Hkv, L, d_pad] row-major, vt [B*Hkv, d_pad,
+ * l_pad] (per-head V^T), padding zero; rows >= seq_lens[b] are excluded from
+ * the amax and written 0.  Slots (amax_bits / counters / scales, each
+ * B*H + 2*B*Hkv long; amax_bits and counters caller-zeroed) are Q heads, then
+ * K heads, then V heads.  Results are bit-identical to ia_quant_amax_rows +
+ * ia_quant_scales + ia_quantize; each f32 element is read from HBM once. */
+int ia_quant_heads(const float* q, const float* k, const float* v, int64_t B, int64_t H,
+                   int64_t Hkv, int64_t L, int64_t d, const int32_t* seq_lens, int8_t* qhat,
+                   int8_t* khat, int8_t* vt, int64_t d_pad, int64_t l_pad, uint32_t* amax_bits,
+                   int32_t* counters, float* scales, int32_t* err_flag, void* stream);
 /* out = f32(values) * scale (quantize.py:126-128), same scale indexing. */
 int ia_dequantize(const int8_t* values, int64_t rows, int64_t cols, int mode,
                   int64_t group, const float* scales, float* out, void* stream);

@@ -1,0 +1,239 @@
+// quant_heads.cu -- per-head dynamic INT8 quantisation of Q, K and V in one launch
+// (reference quantize_symmetric, quantize.py:104-123, called three times per head by
+// int_attention, pipeline.py:217-219).
+//
+// The two-kernel path (quantize.cu: grid-wide amax, then quantise) reads every f32
+// element from HBM twice.  Here a team of CTAs owns one head slab at a time:
+//   pass A: max |x| over the slab's valid rows (HBM read), folded into the slab's
+//           amax slot; the team meets at a per-slab arrival counter;
+//   pass B: s = max(amax, 1e-12f) / 127f and the quantise pass, re-reading the slab
+//           from L2 (teams x slab bytes is kept ~64 MB, under the 126 MB L2).
+// Q^ / K^ are written row-major [L, d_pad] and V^ as the per-head transpose
+// [d_pad, l_pad] the fused kernel's P.V operand wants; padding rows / columns are 0.
+// Arithmetic is the same IEEE f32 sequence as quantize.cu (bit-identical results).
+#include <cstdint>
+
+#include "common.cuh"
+
+namespace ia {
+
+namespace {
+
+__device__ __forceinline__ float qh_scale(uint32_t amax_bits) {
+  return __fdiv_rn(fmaxf(__uint_as_float(amax_bits), 1e-12f), 127.0f);  // quantize.py:113
+}
+__device__ __forceinline__ uint32_t qh_q(float x, float s) {
+  const float t = __fdiv_rn(x, s);               // quantize.py:121
+  float r = floorf(__fadd_rn(fabsf(t), 0.5f));   // rounding.py:21
+  r = fminf(r, 127.0f);                          // quantize.py:122
+  const int v = (int)r;
+  return (uint32_t)(uint8_t)(int8_t)(t < 0.0f ? -v : v);
+}
+__device__ __forceinline__ uint32_t qh_pack4(float4 v, float s) {
+  return qh_q(v.x, s) | (qh_q(v.y, s) << 8) | (qh_q(v.z, s) << 16) | (qh_q(v.w, s) << 24);
+}
+__device__ __forceinline__ uint32_t qh_abs(float x) { return __float_as_uint(x) & 0x7fffffffu; }
+
+struct QHArgs {
+  const float* x[3];
+  int8_t* out[3];
+  int64_t ngroups[3];  // head slabs per tensor
+  int64_t valid_div[3];
+  int transpose[3];
+  int64_t L, d, d_pad, l_pad;
+  const int32_t* valid_rows;
+  uint32_t* amax;   // [n_slabs], caller-zeroed
+  int32_t* count;   // [n_slabs], caller-zeroed
+  float* scales;    // [n_slabs]
+  int32_t* err;
+  int64_t n_slabs;
+  int n_teams, team;
+};
+
+constexpr int QH_THREADS = 512;
+constexpr int QH_TILE_PITCH = 64 + 16;  // transpose tile row pitch (bytes)
+
+__global__ void __launch_bounds__(QH_THREADS) quant_heads_kernel(const QHArgs a) {
+  __shared__ uint32_t red[QH_THREADS / 32];
+  __shared__ float s_sh;
+  extern __shared__ __align__(16) uint8_t tile[];  // [d_pad][QH_TILE_PITCH] (V^T blocks)
+  const int T = a.team;
+  const int team = blockIdx.x / T, rank = blockIdx.x - (blockIdx.x / T) * T;
+  const int tid = threadIdx.x;
+  const int64_t L = a.L, d = a.d;
+  const int64_t d4 = d >> 2;
+  for (int64_t s = team; s < a.n_slabs; s += a.n_teams) {
+    int ti = 0;
+    int64_t g = s;
+    while (ti < 2 && g >= a.ngroups[ti]) { g -= a.ngroups[ti]; ++ti; }
+    int64_t nvalid = L;
+    if (a.valid_rows) {
+      const int64_t v = a.valid_rows[g / a.valid_div[ti]];
+      nvalid = v < 0 ? 0 : (v < L ? v : L);
+    }
+    const float4* base = reinterpret_cast<const float4*>(a.x[ti] + g * L * d);
+    // ---- pass A: max |x| over the valid rows (quantize.py:92-101)
+    const int64_t n4 = nvalid * d4;
+    uint32_t m = 0;
+    {
+      // four independent 16-byte loads in flight per thread (HBM needs the MLP)
+      const int64_t step = (int64_t)T * QH_THREADS;
+      int64_t i = (int64_t)rank * QH_THREADS + tid;
+      for (; i + 3 * step < n4; i += 4 * step) {
+        const float4 v0 = __ldg(base + i), v1 = __ldg(base + i + step);
+        const float4 v2 = __ldg(base + i + 2 * step), v3 = __ldg(base + i + 3 * step);
+        m = max(m, max(max(qh_abs(v0.x), qh_abs(v0.y)), max(qh_abs(v0.z), qh_abs(v0.w))));
+        m = max(m, max(max(qh_abs(v1.x), qh_abs(v1.y)), max(qh_abs(v1.z), qh_abs(v1.w))));
+        m = max(m, max(max(qh_abs(v2.x), qh_abs(v2.y)), max(qh_abs(v2.z), qh_abs(v2.w))));
+        m = max(m, max(max(qh_abs(v3.x), qh_abs(v3.y)), max(qh_abs(v3.z), qh_abs(v3.w))));
+      }
+      for (; i < n4; i += step) {
+        const float4 v = __ldg(base + i);
+        m = max(m, max(max(qh_abs(v.x), qh_abs(v.y)), max(qh_abs(v.z), qh_abs(v.w))));
+      }
+    }
+    m = warp_max_u32(m);
+    if ((tid & 31) == 0) red[tid >> 5] = m;
+    __syncthreads();
+    if (tid < 32) {
+      m = tid < QH_THREADS / 32 ? red[tid] : 0u;
+      m = warp_max_u32(m);
+      if (tid == 0) {
+        // NaN bit patterns sort above +inf: a non-finite element lifts m >= 0x7f800000
+        if (m >= 0x7f800000u) atomicOr(reinterpret_cast<unsigned int*>(a.err), 1u);
+        else if (m) atomicMax(a.amax + s, m);
+        __threadfence();
+        atomicAdd(a.count + s, 1);
+        // the team meets here: every CTA of the team is resident (grid <= occupancy)
+        while (*reinterpret_cast<volatile int32_t*>(a.count + s) < T) __nanosleep(128);
+        __threadfence();
+        const float sc = qh_scale(*reinterpret_cast<volatile uint32_t*>(a.amax + s));
+        s_sh = sc;
+        if (rank == 0) a.scales[s] = sc;
+      }
+    }
+    __syncthreads();
+    const float sc = s_sh;
+    // ---- pass B: quantise (slab re-read from L2)
+    if (!a.transpose[ti]) {
+      const int cpr = (int)(a.d_pad >> 4);  // 16-byte output chunks per row
+      int8_t* og = a.out[ti] + g * L * a.d_pad;
+      const int64_t nch = L * cpr;
+      for (int64_t j = (int64_t)rank * QH_THREADS + tid; j < nch; j += (int64_t)T * QH_THREADS) {
+        const int64_t r = j / cpr;
+        const int c0 = (int)(j - r * cpr) << 4;
+        uint4 o = make_uint4(0u, 0u, 0u, 0u);
+        if (r < nvalid && c0 < d) {
+          const float4* xr = base + r * d4 + (c0 >> 2);
+          if (c0 + 16 <= d) {
+            const float4 v0 = __ldg(xr), v1 = __ldg(xr + 1), v2 = __ldg(xr + 2), v3 = __ldg(xr + 3);
+            o = make_uint4(qh_pack4(v0, sc), qh_pack4(v1, sc), qh_pack4(v2, sc), qh_pack4(v3, sc));
+          } else {
+            uint32_t w[4] = {0u, 0u, 0u, 0u};
+            for (int e = 0; e < 4 && c0 + 4 * e < d; ++e) w[e] = qh_pack4(__ldg(xr + e), sc);
+            o = make_uint4(w[0], w[1], w[2], w[3]);
+          }
+        }
+        *reinterpret_cast<uint4*>(og + r * a.d_pad + c0) = o;
+      }
+    } else {
+      // V^T: 64-key blocks, quantised along d, transposed through smem, stored as
+      // 16-byte runs of keys for each of the d_pad output rows
+      int8_t* og = a.out[ti] + g * a.d_pad * a.l_pad;
+      const int nblk = (int)((a.l_pad + 63) >> 6);
+      const int dp = (int)a.d_pad;
+      for (int rb = rank; rb < nblk; rb += T) {
+        const int64_t r0 = (int64_t)rb * 64;
+        const int nld = 64 * (dp >> 2);  // float4 loads per block (<= 4096)
+        for (int t0 = 0; t0 < nld; t0 += 4 * QH_THREADS) {
+          float4 x4[4];
+          bool ok[4];
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {  // all loads in flight before any use
+            const int t = t0 + u * QH_THREADS + tid;
+            const int rr = t / (dp >> 2), c4 = (t - rr * (dp >> 2)) << 2;
+            ok[u] = t < nld && r0 + rr < nvalid && c4 < d;
+            x4[u] = ok[u] ? __ldg(base + (r0 + rr) * d4 + (c4 >> 2)) : make_float4(0.f, 0.f, 0.f, 0.f);
+          }
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            const int t = t0 + u * QH_THREADS + tid;
+            if (t < nld) {
+              const int rr = t / (dp >> 2), c4 = (t - rr * (dp >> 2)) << 2;
+              const uint32_t q = ok[u] ? qh_pack4(x4[u], sc) : 0u;
+              tile[(c4 + 0) * QH_TILE_PITCH + rr] = (uint8_t)q;
+              tile[(c4 + 1) * QH_TILE_PITCH + rr] = (uint8_t)(q >> 8);
+              tile[(c4 + 2) * QH_TILE_PITCH + rr] = (uint8_t)(q >> 16);
+              tile[(c4 + 3) * QH_TILE_PITCH + rr] = (uint8_t)(q >> 24);
+            }
+          }
+        }
+        __syncthreads();
+        for (int t = tid; t < dp * 4; t += QH_THREADS) {
+          const int c = t >> 2, u = (t & 3) << 4;
+          const int64_t r = r0 + u;
+          if (r < a.l_pad) {
+            const uint32_t* tw = reinterpret_cast<const uint32_t*>(tile + c * QH_TILE_PITCH + u);
+            *reinterpret_cast<uint4*>(og + (int64_t)c * a.l_pad + r) = make_uint4(tw[0], tw[1], tw[2], tw[3]);
+          }
+        }
+        __syncthreads();
+      }
+    }
+    __syncthreads();
+  }
+}
+
+}  // namespace
+}  // namespace ia
+
+using namespace ia;
+
+extern "C" int ia_quant_heads(const float* q, const float* k, const float* v, int64_t B, int64_t H,
+                              int64_t Hkv, int64_t L, int64_t d, const int32_t* seq_lens,
+                              int8_t* qhat, int8_t* khat, int8_t* vt, int64_t d_pad, int64_t l_pad,
+                              uint32_t* amax_bits, int32_t* counters, float* scales,
+                              int32_t* err_flag, void* stream) {
+  if (!q || !k || !v || !qhat || !khat || !vt || !amax_bits || !counters || !scales || !err_flag)
+    return fail(IA_ERR_INVALID_ARGUMENT, "ia_quant_heads: null pointer");
+  if (B < 1 || H < 1 || Hkv < 1 || H % Hkv || L < 1 || d < 1)
+    return fail(IA_ERR_INVALID_ARGUMENT, "ia_quant_heads: bad shape");
+  if ((d & 3) || d > IA_FUSED_MAX_HEAD_DIM || d_pad < d || (d_pad & 15) || d_pad > 256 ||
+      l_pad < L || (l_pad & 15))
+    return fail(IA_ERR_INVALID_ARGUMENT,
+                "ia_quant_heads: needs d %% 4 == 0, d <= d_pad <= 256, d_pad and l_pad %% 16 == 0");
+  if ((((uintptr_t)q | (uintptr_t)k | (uintptr_t)v | (uintptr_t)qhat | (uintptr_t)khat |
+        (uintptr_t)vt) & 15))
+    return fail(IA_ERR_INVALID_ARGUMENT, "ia_quant_heads: operands must be 16-byte aligned");
+  QHArgs a;
+  a.x[0] = q; a.x[1] = k; a.x[2] = v;
+  a.out[0] = qhat; a.out[1] = khat; a.out[2] = vt;
+  a.ngroups[0] = B * H; a.ngroups[1] = B * Hkv; a.ngroups[2] = B * Hkv;
+  a.valid_div[0] = H; a.valid_div[1] = Hkv; a.valid_div[2] = Hkv;
+  a.transpose[0] = 0; a.transpose[1] = 0; a.transpose[2] = 1;
+  a.L = L; a.d = d; a.d_pad = d_pad; a.l_pad = l_pad;
+  a.valid_rows = seq_lens;
+  a.amax = amax_bits; a.count = counters; a.scales = scales; a.err = err_flag;
+  a.n_slabs = B * H + 2 * B * Hkv;
+  const size_t smem = (size_t)d_pad * QH_TILE_PITCH;
+  int per_sm = 0;
+  cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, quant_heads_kernel,
+                                                                QH_THREADS, smem);
+  if (e != cudaSuccess || per_sm < 1) return fail(IA_ERR_CUDA, "ia_quant_heads: occupancy query");
+  // Team barriers need every CTA resident: the grid never exceeds one full wave.
+  const int64_t grid_max = (int64_t)num_sms() * per_sm;
+  const int64_t slab_bytes = L * d * 4;
+  const int64_t slab_elems = L * d;
+  int64_t target = (64ll << 20) / (slab_bytes > 0 ? slab_bytes : 1);  // slabs in flight (~64 MB)
+  target = target < 1 ? 1 : (target > a.n_slabs ? a.n_slabs : target);
+  int64_t team = grid_max / target;
+  const int64_t want = (slab_elems + QH_THREADS * 16 - 1) / (QH_THREADS * 16);  // >= 16 elem/thread
+  team = team < want ? team : want;
+  team = team < 1 ? 1 : team;
+  int64_t n_teams = grid_max / team;
+  n_teams = n_teams > a.n_slabs ? a.n_slabs : n_teams;
+  a.n_teams = (int)n_teams;
+  a.team = (int)team;
+  quant_heads_kernel<<<(unsigned)(n_teams * team), QH_THREADS, smem, (cudaStream_t)stream>>>(a);
+  return check_launch("quant_heads_kernel");
+}

@@ -67,12 +67,14 @@ class QuantOut:
 
 
 class Workspace:
-    """Per-call scratch: amax bit slots (zeroed) + the non-finite flag."""
+    """Per-call scratch: amax bit slots and team arrival counters (both zeroed)
+    + the non-finite flag."""
 
     def __init__(self, n_slots: int, device):
-        self.buf = torch.zeros(n_slots + 1, dtype=torch.int32, device=device)
+        self.buf = torch.zeros(2 * n_slots + 1, dtype=torch.int32, device=device)
         self.amax = self.buf[:n_slots]
-        self.err = self.buf[n_slots:]
+        self.count = self.buf[n_slots:2 * n_slots]
+        self.err = self.buf[2 * n_slots:]
         self.scales = torch.empty(n_slots, dtype=torch.float32, device=device)
         self._off = 0
 
@@ -142,12 +144,15 @@ HEAD_PARAMS_BYTES = ctypes.sizeof(_lib.HeadParams)
 
 
 def prepare(q, k, v, *, seq_lens=None, scale_granularity="head", b=5, c=6.6, p_scale=255,
-            d_pad=None, scales=None) -> Prepared:
+            d_pad=None, scales=None, quant="fused") -> Prepared:
     """Quantise Q/K/V on device and compute per-(b, h) parameters.
 
     ``scales`` (optional): precomputed global (q, k, v) f32 scales as 1-element
     device tensors -- the sharded launcher's all-reduced amax; implies
     ``scale_granularity="tensor"`` and skips the amax kernels.
+    ``quant``: "fused" (default) quantises per-head Q/K/V in one launch
+    (ia_quant_heads) when the layout allows; "split" forces the amax +
+    quantise kernels (bit-identical; kept for A/B checks).
     """
     B, H, Lq, d = q.shape
     Hkv = k.shape[1]
@@ -163,6 +168,18 @@ def prepare(q, k, v, *, seq_lens=None, scale_granularity="head", b=5, c=6.6, p_s
     ak, sk = ws.take(nkv)
     av, sv = ws.take(nkv)
     sl = seq_lens
+    qhat = torch.empty((B * H, Lq, d_pad), dtype=torch.int8, device=dev)
+    khat = torch.empty((B * Hkv, Lq, d_pad), dtype=torch.int8, device=dev)
+    vt = torch.empty((B * Hkv, d_pad, l_pad), dtype=torch.int8, device=dev)
+    if quant == "fused" and per_head and d % 4 == 0 and d_pad <= 256 and d_pad % 16 == 0 and all(
+            t.is_contiguous() and t.data_ptr() % 16 == 0 for t in (q, k, v)):
+        # one launch: per-head amax + quantise of Q, K, V (f32 read from HBM once)
+        _lib.check(_lib.load().ia_quant_heads(
+            _p(q), _p(k), _p(v), B, H, Hkv, Lq, d, _p(sl), _p(qhat), _p(khat), _p(vt), d_pad,
+            l_pad, _p(ws.amax), _p(ws.count), _p(ws.scales), _p(ws.err), _stream()),
+            "quantize heads")
+        return _finish_prepare(qhat, khat, vt, sq, sk, sv, ws, per_head, B, H, Hkv, d, b, c,
+                               p_scale, d_pad, l_pad)
     if scales is None:
         amax_rows(q, B * H, Lq, d, aq, ws.err, seq_lens=sl, valid_div=H,
                   slot_div=1 if per_head else B * H)
@@ -174,16 +191,19 @@ def prepare(q, k, v, *, seq_lens=None, scale_granularity="head", b=5, c=6.6, p_s
     else:
         for dst, src in zip((sq, sk, sv), scales):
             dst.copy_(src.reshape(1))
-    qhat = torch.empty((B * H, Lq, d_pad), dtype=torch.int8, device=dev)
-    khat = torch.empty((B * Hkv, Lq, d_pad), dtype=torch.int8, device=dev)
-    vt = torch.empty((B * Hkv, d_pad, l_pad), dtype=torch.int8, device=dev)
     quantize_rows(q, B * H, Lq, d, sq, qhat, d_pad, seq_lens=sl, valid_div=H,
                   slot_div=1 if per_head else B * H)
     quantize_rows(k, B * Hkv, Lq, d, sk, khat, d_pad, seq_lens=sl, valid_div=Hkv,
                   slot_div=1 if per_head else B * Hkv)
     quantize_vt(v, B * Hkv, Lq, d, sv, vt, l_pad, d_pad * l_pad, seq_lens=sl, valid_div=Hkv,
                 slot_div=1 if per_head else B * Hkv)
-    params = torch.empty((B * H, HEAD_PARAMS_BYTES), dtype=torch.uint8, device=dev)
+    return _finish_prepare(qhat, khat, vt, sq, sk, sv, ws, per_head, B, H, Hkv, d, b, c, p_scale,
+                           d_pad, l_pad)
+
+
+def _finish_prepare(qhat, khat, vt, sq, sk, sv, ws, per_head, B, H, Hkv, d, b, c, p_scale, d_pad,
+                    l_pad) -> Prepared:
+    params = torch.empty((B * H, HEAD_PARAMS_BYTES), dtype=torch.uint8, device=qhat.device)
     _lib.check(_lib.load().ia_head_params_dev(_p(sq), _p(sk), _p(sv), int(per_head),
                                               int(per_head), B, H, Hkv, d, float(c), 1 << b,
                                               int(p_scale), _p(params), _stream()), "head params")

@@ -210,3 +210,40 @@ def test_sharded_single_rank_gpu_tensor_scales():
     out, _ = sharding.sharded_attention(q, k, v, causal=True, scale_granularity="tensor")
     want, _ = O.attention_batched(q, k, v, causal=True, scale_granularity="tensor")
     assert np.array_equal(out.view(np.uint32), want.view(np.uint32)), _first_diff(out, want)
+
+
+@pytest.mark.parametrize("B,H,Hkv,L,d,lens", [
+    (1, 1, 1, 128, 64, None), (2, 4, 2, 333, 128, [333, 100]), (1, 2, 1, 77, 20, None),
+    (3, 2, 2, 1000, 64, [1000, 0, 513]), (1, 8, 2, 4100, 128, None), (1, 1, 1, 64, 256, None),
+    (1, 2, 2, 200, 36, [150])])
+def test_quant_heads_matches_split(B, H, Hkv, L, d, lens):
+    """ia_quant_heads (one launch, team barriers) is bit-identical to the split
+    amax + quantise kernels: Q^, K^, V^T (incl. padding) and every scale."""
+    rng = np.random.default_rng(B * 1000 + L + d)
+    dev = torch.device("cuda", 0)
+    q = torch.from_numpy(rng.standard_normal((B, H, L, d), dtype=np.float32) * 3).to(dev)
+    k = torch.from_numpy(rng.standard_normal((B, Hkv, L, d), dtype=np.float32)).to(dev)
+    v = torch.from_numpy(rng.standard_normal((B, Hkv, L, d), dtype=np.float32) * 0.1).to(dev)
+    sl = None
+    if lens is not None:
+        lens = (lens * B)[:B]
+        sl = torch.tensor(lens, dtype=torch.int32, device=dev)
+    a = E.prepare(q, k, v, seq_lens=sl, quant="fused")
+    b = E.prepare(q, k, v, seq_lens=sl, quant="split")
+    for x, y, nm in [(a.qhat, b.qhat, "qhat"), (a.khat, b.khat, "khat"), (a.vt, b.vt, "vt"),
+                     (a.q_scales, b.q_scales, "sq"), (a.k_scales, b.k_scales, "sk"),
+                     (a.v_scales, b.v_scales, "sv"),
+                     (a.params[:, :52], b.params[:, :52], "params")]:  # 52 = defined bytes
+        assert torch.equal(x, y), (nm, _first_diff(x.cpu().numpy(), y.cpu().numpy()))
+    assert int(a.err.item()) == 0
+
+
+def test_quant_heads_nonfinite():
+    dev = torch.device("cuda", 0)
+    q = torch.randn(1, 2, 256, 64, device=dev)
+    k = torch.randn(1, 2, 256, 64, device=dev)
+    v = torch.randn(1, 2, 256, 64, device=dev)
+    k[0, 1, 17, 3] = float("nan")
+    assert int(E.prepare(q, k, v).err.item()) == 1
+    with pytest.raises(ValueError):
+        ia.int_attention_batched(q, k, v)
