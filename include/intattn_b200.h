@@ -164,6 +164,16 @@ int ia_index_softmax(const int32_t* logits, int64_t rows, int64_t cols,
                      const ia_head_params* hp, const uint8_t* lut, int nlut, int p_scale,
                      const uint8_t* mask, uint8_t* out, void* stream);
 
+/* index_softmax_grouped (softmax.py:309-399, default per-group-max mode):
+ * group_of_column [cols] int32 (device) maps each column to a group in
+ * [0, n_groups), n_groups <= 4096; hp [n_groups] is a DEVICE array of
+ * per-group index-map parameters (ia_softmax_params_host(c_int^(g), ...)).
+ * Masked columns get e = 0; the row normalisation is shared by all groups. */
+int ia_index_softmax_grouped(const int32_t* logits, int64_t rows, int64_t cols,
+                             const int32_t* group_of_column, int n_groups,
+                             const ia_head_params* hp, const uint8_t* lut, int nlut,
+                             int p_scale, const uint8_t* mask, uint8_t* out, void* stream);
+
 /* Exact int8 GEMM on tcgen05 (matmul_int8 / gemm_qk / gemm_pv, gemm.py:45-133):
  * C[M, N] int32 = A[M, K] * B[N, K]^T; A is s8 (a_signed = 1) or u8; B is s8.
  * lda/ldb are byte pitches (multiples of 16); ldc in elements. */

@@ -12,8 +12,11 @@ commits its outputs as small fixtures:
   tests/golden/stage_small.npz   full per-stage arrays for a few tiny cases
   tests/golden/configs.json      per-(b, head) scales, c_int and output
                                  digests for the five BASELINE configs
+  tests/golden/grouped_cases.npz index_softmax_grouped (softmax.py:309-399)
+                                 inputs and outputs, incl. the grouped-K
+                                 int_attention pipeline (pipeline.py:229-246)
 
-Usage:  python oracle/gen_golden.py [--configs C1,C2,...] [--skip-stages]
+Usage:  python oracle/gen_golden.py [--configs C1,C2,...] [--skip-stages] [--grouped-only]
 The reference is imported read-only: bytecode writing is disabled and numba's
 cache is redirected to a temp dir so nothing is written under /root/reference.
 """
@@ -183,13 +186,74 @@ def config_golden(name, threads):
                 c_int=cis, ref_seconds=time.time() - t0, ref_threads=threads)
 
 
+def grouped_cases():
+    """Grouped-key IndexSoftmax straight from the reference: random int32 logits,
+    contiguous and scattered column groups, masks, both P formats; plus the
+    per-row-group-K int_attention pipeline end to end."""
+    rng = np.random.default_rng(2511)
+    out = {}
+    lut = ref_sm.build_lut(5, 6.6)
+    n_sm = 0
+    for L, ng, contiguous, mask_kind, pf in [
+            (64, 4, True, None, 255), (96, 3, False, None, 255), (80, 5, True, "causal", 255),
+            (72, 2, False, "random", 127), (48, 1, True, None, 255), (128, 8, True, "causal", 127),
+            (33, 6, False, "rowdead", 255)]:
+        logits = rng.integers(-200000, 200000, size=(L, L)).astype(np.int32)
+        if contiguous:
+            groups = np.repeat(np.arange(ng), (L + ng - 1) // ng)[:L]
+        else:
+            groups = rng.integers(0, ng, size=L)
+            groups[:ng] = np.arange(ng)
+        alphas = (rng.uniform(0.2, 30.0, size=ng) / 1000.0).tolist()
+        mask = None
+        if mask_kind == "causal":
+            mask = np.triu(np.ones((L, L), bool), 1)
+        elif mask_kind == "random":
+            mask = rng.random((L, L)) < 0.3
+        elif mask_kind == "rowdead":
+            mask = rng.random((L, L)) < 0.2
+            mask[5, :] = True
+        fmt = ref_sm.PFormat.UINT8X255 if pf == 255 else ref_sm.PFormat.INT8X127
+        prob = ref_sm.index_softmax_grouped(ref_sm.np.asarray(logits), groups, alphas, 6.6, lut,
+                                            mask=mask, p_format=fmt)
+        key = f"sm{n_sm}"
+        out[key + "_logits"] = logits
+        out[key + "_groups"] = groups.astype(np.int32)
+        out[key + "_alphas"] = np.array(alphas, np.float64)
+        out[key + "_mask"] = np.zeros((0, 0), bool) if mask is None else mask
+        out[key + "_pf"] = np.array(pf)
+        out[key + "_prob"] = np.asarray(prob.values).view(np.uint8)
+        n_sm += 1
+    out["n_sm"] = np.array(n_sm)
+    n_pipe = 0
+    for L, d, gs, causal in [(96, 32, 32, False), (128, 64, 16, True), (70, 20, 7, False)]:
+        q = rng.standard_normal((L, d), dtype=np.float32)
+        k = rng.standard_normal((L, d), dtype=np.float32) * rng.uniform(0.5, 4.0, size=(L, 1)).astype(np.float32)
+        v = rng.standard_normal((L, d), dtype=np.float32)
+        mask = np.triu(np.ones((L, L), bool), 1) if causal else None
+        cfg = ia.AttentionConfig(granularity=ia.QuantGranularity.per_row_group(gs), mask=mask)
+        o, _ = ia.int_attention(q, k, v, cfg)
+        key = f"pipe{n_pipe}"
+        out[key + "_q"], out[key + "_k"], out[key + "_v"] = q, k, v
+        out[key + "_gs"] = np.array(gs)
+        out[key + "_causal"] = np.array(int(causal))
+        out[key + "_out"] = np.asarray(o, np.float32)
+        n_pipe += 1
+    out["n_pipe"] = np.array(n_pipe)
+    np.savez_compressed(os.path.join(GOLD, "grouped_cases.npz"), **out)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--configs", default="C1,C2,C2h,C3,C4,C5")
     ap.add_argument("--skip-stages", action="store_true")
     ap.add_argument("--threads", type=int, default=os.cpu_count())
+    ap.add_argument("--grouped-only", action="store_true")
     a = ap.parse_args()
     os.makedirs(GOLD, exist_ok=True)
+    grouped_cases()
+    if a.grouped_only:
+        return
     with open(os.path.join(GOLD, "kats.json"), "w") as f:
         json.dump(kats(), f, indent=1)
     if not a.skip_stages:

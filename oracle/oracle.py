@@ -190,3 +190,39 @@ def attention_batched(q, k, v, *, causal=False, seq_lens=None, mask=None,
     if st != 0:
         raise ValueError(f"oracle rejected arguments (status {st})")
     return out, {"q_scales": qs, "k_scales": ks, "v_scales": vs, "c_int": ci}
+
+
+def index_softmax_grouped(logits: np.ndarray, groups: np.ndarray, c_ints, lut: np.ndarray,
+                          mask=None, p_scale=P_UINT8X255) -> np.ndarray:
+    """Grouped-key IndexSoftmax, default per-group-max mode (softmax.py:309-399):
+    per group g a row max over the row's unmasked columns of g and the clip
+    threshold c_ints[g]; e = lut[(2k min(m_g - a, c_g) + c_g) // (2c_g)], masked
+    e = 0; shared row normalisation (2 scale e + s) // max(2s, 1)
+    (softmax.py:300-306).  Plain int64 numpy; returns u8 (i8 bytes for 127)."""
+    v = np.asarray(logits).astype(np.int64)
+    groups = np.asarray(groups).astype(np.int64)
+    lut = np.asarray(lut).astype(np.int64)
+    k = len(lut) - 1
+    m8 = None if mask is None else np.asarray(mask, bool)
+    e = np.zeros(v.shape, np.int64)
+    for g, ci in enumerate(c_ints):
+        cols = np.flatnonzero(groups == g)
+        if cols.size == 0:
+            continue
+        sub = v[:, cols]
+        work = np.where(m8[:, cols], -(1 << 62), sub) if m8 is not None else sub
+        m = work.max(axis=1)
+        dl = np.minimum(np.maximum(m[:, None] - sub, 0), ci)
+        e[:, cols] = lut[(2 * dl * k + ci) // (2 * ci)]
+    if m8 is not None:
+        e[m8] = 0
+    s = e.sum(axis=1)
+    out = (e * (2 * p_scale) + s[:, None]) // np.maximum(2 * s, 1)[:, None]
+    return out.astype(np.uint8)
+
+
+def c_int_from_alpha(c: float, alpha: float) -> int:
+    """max(1, min(round_half_away(c / alpha), 2^52)) in f64 (softmax.py:105-108)."""
+    r = float(c) / float(alpha)
+    ci = int(np.copysign(np.floor(abs(r) + 0.5), r))
+    return max(1, min(ci, 1 << 52))

@@ -32,7 +32,8 @@ EXPORTS = (
     "ia_abi_version", "ia_status_string", "ia_last_error", "ia_device_check",
     "ia_quant_amax_rows", "ia_quant_amax_cols", "ia_quant_scales", "ia_quantize",
     "ia_dequantize", "ia_quant_heads", "ia_head_params_host", "ia_softmax_params_host", "ia_head_params_dev",
-    "ia_mask_pack", "ia_attn_fwd", "ia_attn_supported", "ia_index_softmax", "ia_gemm_i8",
+    "ia_mask_pack", "ia_attn_fwd", "ia_attn_supported", "ia_index_softmax", "ia_index_softmax_grouped",
+    "ia_gemm_i8",
 )
 
 
@@ -105,6 +106,7 @@ def load():
             "ia_attn_fwd": ([ctypes.POINTER(AttnArgs), P], i32),
             "ia_attn_supported": ([i64, i32], i32),
             "ia_index_softmax": ([P, i64, i64, ctypes.POINTER(HeadParams), P, i32, i32, P, P, P], i32),
+            "ia_index_softmax_grouped": ([P, i64, i64, P, i32, P, P, i32, i32, P, P, P], i32),
             "ia_gemm_i8": ([P, i64, i32, P, i64, i64, i64, i64, P, i64, P], i32),
         }
         for name, (args, res) in sig.items():

@@ -328,6 +328,26 @@ def index_softmax_dev(logits, c_int, lut, mask=None, p_scale=255, delta_bound=(1
     return out
 
 
+def index_softmax_grouped_dev(logits, groups, c_ints, lut, mask=None, p_scale=255,
+                              delta_bound=(1 << 32) - 1):
+    """Grouped-key IndexSoftmax kernel (ia_index_softmax_grouped); ``groups`` is an
+    int array [cols], ``c_ints`` the per-group clip thresholds."""
+    rows, cols = logits.shape
+    dev = logits.device
+    lut_t = torch.as_tensor(np.ascontiguousarray(lut, np.uint8)).to(dev)
+    hps = (_lib.HeadParams * len(c_ints))()
+    for i, ci in enumerate(c_ints):
+        hps[i] = _lib.softmax_params_host(int(ci), delta_bound, len(lut))
+    hp_t = torch.frombuffer(bytearray(bytes(hps)), dtype=torch.uint8).to(dev)
+    g_t = torch.as_tensor(np.ascontiguousarray(groups, np.int32)).to(dev)
+    m8 = None if mask is None else mask.to(torch.uint8).contiguous()
+    out = torch.empty((rows, cols), dtype=torch.uint8, device=dev)
+    _lib.check(_lib.load().ia_index_softmax_grouped(
+        _p(logits), rows, cols, _p(g_t), len(c_ints), _p(hp_t), _p(lut_t), len(lut), int(p_scale),
+        _p(m8), _p(out), _stream()), "index_softmax_grouped")
+    return out
+
+
 def _attention_unfused(q, k, v, *, causal, seq_lens, mask, scale_granularity, b, c, p_scale,
                        lut, out, check_finite):
     """d > 256: per-unit stage kernels (tcgen05 GEMM -> row IndexSoftmax -> tcgen05 GEMM)."""

@@ -169,9 +169,12 @@ def index_softmax_grouped(logits, group_of_column, alphas, c, lut, mask=None,
     """Grouped-key IndexSoftmax (softmax.py:302-399): per-group clip threshold
     c_int^(g) = max(1, round(c / alpha_g)) and, by default, a per-group row max.
 
-    Composed from exact int64 / f64 torch ops on the device (a SURVEY §8f
-    "next" row; no dedicated kernel yet).  A single group is bit-identical to
-    ``index_softmax``.
+    The default (per-group max) mode runs the grouped row kernel
+    (csrc/softmax_rows.cu, ia_index_softmax_grouped; <= 4096 groups).  The
+    diagnostic ``common_max`` mode (f64 rescaling onto the finest group's grid,
+    "not part of the integer runtime path", softmax.py:324-326) and > 4096
+    groups are composed from exact int64 / f64 torch ops on the device.  A single
+    group is bit-identical to ``index_softmax``.
     """
     values = _logit_values(logits)
     _check_lut(lut)
@@ -191,6 +194,16 @@ def index_softmax_grouped(logits, group_of_column, alphas, c, lut, mask=None,
     if groups.min() < 0 or groups.max() >= len(alphas):
         raise ValueError("every column must map to a group in [0, len(alphas))")
     dev = v.device
+    if not common_max and len(alphas) <= 4096:
+        m = _prep_mask(mask, v.shape) if mask is not None else None
+        cis = [min(_c_int_from_alpha(c, a), _C_INT_CAP) for a in alphas]
+        _note("surrogates", np.uint8)
+        out = E.index_softmax_grouped_dev(to_device(values, np.int32), groups, cis, lut.entries,
+                                          m, p_format.value)
+        if p_format is PFormat.INT8X127:
+            out = out.view(torch.int8)
+        _note("prob", np.int8 if p_format is PFormat.INT8X127 else np.uint8)
+        return ProbMatrix(values=to_host(out, numpy_in), denom_scale=p_format.value)
     k = len(lut.entries) - 1
     lut_t = torch.as_tensor(lut.entries.astype(np.int64), device=dev)
     m8 = _prep_mask(mask, v.shape) if mask is not None else None

@@ -247,3 +247,55 @@ def test_quant_heads_nonfinite():
     assert int(E.prepare(q, k, v).err.item()) == 1
     with pytest.raises(ValueError):
         ia.int_attention_batched(q, k, v)
+
+
+def _grouped_gold():
+    import os
+    return np.load(os.path.join(os.path.dirname(__file__), "golden", "grouped_cases.npz"))
+
+
+def test_grouped_softmax_kernel_golden():
+    """ia_index_softmax_grouped vs the reference's own index_softmax_grouped outputs."""
+    G = _grouped_gold()
+    lut = ia.build_lut(5, 6.6)
+    for i in range(int(G["n_sm"])):
+        key = f"sm{i}"
+        mask = G[key + "_mask"]
+        mask = None if mask.size == 0 else mask
+        pf = ia.PFormat.UINT8X255 if int(G[key + "_pf"]) == 255 else ia.PFormat.INT8X127
+        got = ia.index_softmax_grouped(G[key + "_logits"], G[key + "_groups"],
+                                       list(G[key + "_alphas"]), 6.6, lut, mask=mask, p_format=pf)
+        assert np.array_equal(np.asarray(got.values).view(np.uint8), G[key + "_prob"]), key
+
+
+@pytest.mark.parametrize("L,ng,masked", [(300, 7, False), (1024, 16, True), (2000, 1, True),
+                                         (517, 600, False)])
+def test_grouped_softmax_kernel_random(L, ng, masked):
+    """Grouped kernel vs the oracle restatement on larger seeded cases (incl. many
+    tiny groups and a single group, which must equal plain index_softmax)."""
+    rng = np.random.default_rng(L + ng)
+    logits = rng.integers(-2_000_000, 2_000_000, size=(L, L)).astype(np.int32)
+    groups = rng.integers(0, ng, size=L).astype(np.int32)
+    alphas = list(rng.uniform(1e-5, 5e-2, size=ng))
+    mask = np.triu(np.ones((L, L), bool), 1) if masked else None
+    lut = ia.build_lut(5, 6.6)
+    got = np.asarray(ia.index_softmax_grouped(logits, groups, alphas, 6.6, lut, mask=mask).values)
+    cis = [O.c_int_from_alpha(6.6, a) for a in alphas]
+    want = O.index_softmax_grouped(logits, groups, cis, lut.entries, mask)
+    assert np.array_equal(got, want), _first_diff(got, want)
+    if ng == 1:
+        plain = np.asarray(ia.index_softmax(logits, cis[0], lut, mask=mask).values)
+        assert np.array_equal(got, plain)
+
+
+def test_grouped_pipeline_golden():
+    """Per-row-group K int_attention (pipeline.py:229-246) end to end vs the reference."""
+    G = _grouped_gold()
+    for i in range(int(G["n_pipe"])):
+        key = f"pipe{i}"
+        L = G[key + "_q"].shape[0]
+        mask = np.triu(np.ones((L, L), bool), 1) if int(G[key + "_causal"]) else None
+        cfg = ia.AttentionConfig(granularity=ia.QuantGranularity.per_row_group(int(G[key + "_gs"])),
+                                 mask=mask)
+        out, _ = ia.int_attention(G[key + "_q"], G[key + "_k"], G[key + "_v"], cfg)
+        assert np.array_equal(np.asarray(out).view(np.uint32), G[key + "_out"].view(np.uint32)), key

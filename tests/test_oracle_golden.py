@@ -143,3 +143,23 @@ def test_configs_bit_exact_long(name):
     if name not in configs():
         pytest.skip("golden for this config not generated")
     _check_config(name)
+
+
+def _grouped():
+    import os
+    return np.load(os.path.join(os.path.dirname(__file__), "golden", "grouped_cases.npz"))
+
+
+def test_oracle_grouped_softmax_matches_reference():
+    """The numpy restatement of index_softmax_grouped equals the reference's
+    own outputs (tests/golden/grouped_cases.npz, oracle/gen_golden.py)."""
+    G = _grouped()
+    lut = O.build_lut(5, 6.6)
+    for i in range(int(G["n_sm"])):
+        key = f"sm{i}"
+        mask = G[key + "_mask"]
+        mask = None if mask.size == 0 else mask
+        cis = [O.c_int_from_alpha(6.6, a) for a in G[key + "_alphas"]]
+        got = O.index_softmax_grouped(G[key + "_logits"], G[key + "_groups"], cis, lut, mask,
+                                      int(G[key + "_pf"]))
+        assert np.array_equal(got, G[key + "_prob"]), key
