@@ -19,7 +19,7 @@
 extern "C" {
 #endif
 
-#define IA_ABI_VERSION 2  /* 2: ia_head_params gained magic9 */
+#define IA_ABI_VERSION 3  /* 2: ia_head_params gained magic9; 3: ia_attn_args.softmax_mode */
 #define IA_MAX_SEQ_LEN 65536   /* gemm.py:26 MAX_SEQ_LEN */
 #define IA_MAX_HEAD_DIM 131070 /* gemm.py:25 MAX_HEAD_DIM */
 #define IA_FUSED_MAX_HEAD_DIM 256
@@ -149,7 +149,13 @@ typedef struct ia_attn_args {
   uint8_t* dbg_prob;   /* optional [B*H, L, L] u8 */
   int32_t* dbg_acc;    /* optional [B*H, L, d_pad] int32 */
   long long* dbg_times; /* optional [grid, 16] int64 per-CTA phase clocks (zeroed; profiling) */
+  int32_t softmax_mode; /* IA_SOFTMAX_INDEX: IndexSoftmax (softmax.py:265-299, bit-exact);
+                           IA_SOFTMAX_FLOAT: the quant-only comparator's dequantise -> f32
+                           softmax -> requantise path (pipeline.py:259-296), with MUFU exp2,
+                           so P^ matches the reference to float tolerance, not bit for bit */
 } ia_attn_args;
+#define IA_SOFTMAX_INDEX 0
+#define IA_SOFTMAX_FLOAT 1
 
 int ia_attn_fwd(const ia_attn_args* args, void* stream);
 /* IA_OK if the fused kernel supports (d_pad, 2^b LUT entries) within shared

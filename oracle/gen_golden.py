@@ -12,6 +12,8 @@ commits its outputs as small fixtures:
   tests/golden/stage_small.npz   full per-stage arrays for a few tiny cases
   tests/golden/configs.json      per-(b, head) scales, c_int and output
                                  digests for the five BASELINE configs
+  tests/golden/quant_only_cases.npz  quant_only_attention (pipeline.py:259-296)
+                                 outputs and requantised P^ (float comparator)
   tests/golden/grouped_cases.npz index_softmax_grouped (softmax.py:309-399)
                                  inputs and outputs, incl. the grouped-K
                                  int_attention pipeline (pipeline.py:229-246)
@@ -243,6 +245,45 @@ def grouped_cases():
     np.savez_compressed(os.path.join(GOLD, "grouped_cases.npz"), **out)
 
 
+def quant_only_cases():
+    """The paper's comparator from the reference: output and the requantised P^
+    (its private _stable_softmax / _quantize_probs, pipeline.py:119-140)."""
+    from intattn import pipeline as ref_pipe
+    import math
+    rng = np.random.default_rng(259)
+    out = {}
+    n = 0
+    for L, d, mask_kind, pf in [(128, 64, None, 255), (300, 128, "causal", 255),
+                                (77, 32, "dead", 255), (200, 64, "causal", 127),
+                                (513, 128, None, 255)]:
+        q = rng.standard_normal((L, d), dtype=np.float32)
+        k = rng.standard_normal((L, d), dtype=np.float32)
+        v = rng.standard_normal((L, d), dtype=np.float32)
+        mask = None
+        if mask_kind == "causal":
+            mask = np.triu(np.ones((L, L), bool), 1)
+        elif mask_kind == "dead":
+            mask = rng.random((L, L)) < 0.25
+            mask[3, :] = True
+        fmt = ia.PFormat.UINT8X255 if pf == 255 else ia.PFormat.INT8X127
+        o, _ = ia.quant_only_attention(q, k, v, ia.AttentionConfig(mask=mask, p_format=fmt))
+        qh = ia.quantize_symmetric(q)
+        kh = ia.quantize_symmetric(k)
+        logits = ia.matmul_int8(qh.values, kh.values)
+        alpha = np.float32(float(qh.scales[0]) * float(kh.scales[0]) / math.sqrt(d))
+        phat = ref_pipe._quantize_probs(ref_pipe._stable_softmax(logits.astype(np.float32) * alpha, mask), fmt)
+        key = f"qo{n}"
+        out[key + "_q"], out[key + "_k"], out[key + "_v"] = q, k, v
+        out[key + "_mask"] = np.zeros((0, 0), bool) if mask is None else mask
+        out[key + "_pf"] = np.array(pf)
+        out[key + "_out"] = np.asarray(o, np.float32)
+        out[key + "_phat"] = np.asarray(phat).view(np.uint8)
+        out[key + "_sv"] = np.array(float(ia.quantize_symmetric(v).scales[0]), np.float32)
+        n += 1
+    out["n"] = np.array(n)
+    np.savez_compressed(os.path.join(GOLD, "quant_only_cases.npz"), **out)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--configs", default="C1,C2,C2h,C3,C4,C5")
@@ -252,6 +293,7 @@ def main():
     a = ap.parse_args()
     os.makedirs(GOLD, exist_ok=True)
     grouped_cases()
+    quant_only_cases()
     if a.grouped_only:
         return
     with open(os.path.join(GOLD, "kats.json"), "w") as f:

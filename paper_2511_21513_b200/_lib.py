@@ -55,7 +55,10 @@ class AttnArgs(ctypes.Structure):
                 ("nlut", ctypes.c_int32), ("p_scale", ctypes.c_int32),
                 ("lut", ctypes.c_uint8 * 256), ("dbg_logits", ctypes.c_void_p),
                 ("dbg_prob", ctypes.c_void_p), ("dbg_acc", ctypes.c_void_p),
-                ("dbg_times", ctypes.c_void_p)]
+                ("dbg_times", ctypes.c_void_p), ("softmax_mode", ctypes.c_int32)]
+
+IA_SOFTMAX_INDEX = 0
+IA_SOFTMAX_FLOAT = 1
 
 
 _lock = threading.Lock()

@@ -20,7 +20,7 @@ from .pipeline import AttentionConfig
 
 def int_attention_batched(q, k, v, *, causal=False, seq_lens=None, mask=None,
                           scale_granularity="head", cfg=None, out=None, debug=False,
-                          check_finite=True):
+                          check_finite=True, softmax="index"):
     """Fused IntAttention over all (b, h) units.
 
     q: [B, H, L, d] f32; k, v: [B, Hkv, L, d] f32 with H % Hkv == 0.
@@ -49,7 +49,7 @@ def int_attention_batched(q, k, v, *, causal=False, seq_lens=None, mask=None,
         raise ValueError("empty attention problem")
     numpy_in = not is_torch(q)
     host_in = all((not is_torch(x)) or x.device.type == "cpu" for x in (q, k, v))
-    if host_in and not debug and scale_granularity == "head" and B * ks[1] > 1:
+    if host_in and not debug and scale_granularity == "head" and B * ks[1] > 1 and softmax == "index":
         return _host_pipelined(q, k, v, causal=causal, seq_lens=seq_lens, mask=mask, cfg=cfg,
                                out=out, check_finite=check_finite, numpy_in=numpy_in)
     qt, kt, vt = (to_device(x, np.float32) for x in (q, k, v))
@@ -68,11 +68,24 @@ def int_attention_batched(q, k, v, *, causal=False, seq_lens=None, mask=None,
     res = E.attention(qt, kt, vt, causal=causal, seq_lens=sl, mask=mt,
                       scale_granularity=scale_granularity, b=cfg.b, c=cfg.c,
                       p_scale=cfg.p_format.value, out=o, debug=debug,
-                      check_finite=check_finite)
+                      check_finite=check_finite, softmax=softmax)
     if debug:
         res, dbg = res
         return to_host(res, numpy_in), dbg
     return to_host(res, numpy_in)
+
+
+def quant_only_attention_batched(q, k, v, *, causal=False, seq_lens=None, mask=None,
+                                 scale_granularity="head", cfg=None, out=None, debug=False,
+                                 check_finite=True):
+    """The paper's comparator over all (b, h) units: the same INT8 QK^T / P.V MMAs
+    with the dequantise -> f32 softmax -> requantise detour of
+    quant_only_attention (pipeline.py:259-296) instead of IndexSoftmax, fused
+    (two passes: online max / sum-of-exp, then P^ and P.V).  exp is MUFU ex2, so
+    P^ matches the reference to float tolerance, not bit for bit."""
+    return int_attention_batched(q, k, v, causal=causal, seq_lens=seq_lens, mask=mask,
+                                 scale_granularity=scale_granularity, cfg=cfg, out=out,
+                                 debug=debug, check_finite=check_finite, softmax="float")
 
 
 def _pinned(x):

@@ -172,7 +172,7 @@ __device__ __forceinline__ void bwait(uint64_t* bar, uint32_t parity, bool spin)
   else mbar_wait(bar, parity);
 }
 
-template <int DP, bool DEBUG, bool SKEL = false>
+template <int DP, bool DEBUG, bool SKEL = false, bool QO = false>
 __global__ void __launch_bounds__(Cfg<DP>::NTHREADS, 1)
     attn_fwd_kernel(const __grid_constant__ CUtensorMap tmq,
                     const __grid_constant__ CUtensorMap tmk,
@@ -227,7 +227,10 @@ __global__ void __launch_bounds__(Cfg<DP>::NTHREADS, 1)
   const int key_end = p.causal ? min(q0 + BM, len) : len;
   const int n_kt = (key_end + BN - 1) / BN;
   const bool resident = n_kt <= NWG;  // every logit tile fits its own TMEM buffer
-  const int npass = resident ? 1 : ((p.xflags & 1) ? 1 : 3);
+  // QO (quant-only comparator, pipeline.py:259-296): an online f32 max / sum-of-exp
+  // pass, then the P / P.V pass -- two passes instead of IndexSoftmax's three.
+  const int npass = resident ? 1 : ((p.xflags & 1) ? 1 : (QO ? 2 : 3));
+  constexpr int PV_PASS = QO ? 1 : 2;  // tile t >= PV_PASS * n_kt belongs to the P / P.V pass
   const int n_kt_b = (p.xflags & 1) ? 0 : n_kt;  // key tiles of passes 2-3 / P.V
 
   if (rw == 0 && lane == 0) {
@@ -280,7 +283,7 @@ __global__ void __launch_bounds__(Cfg<DP>::NTHREADS, 1)
     __syncwarp();
     uint32_t kph = 0;  // per-stage phase bits
     int n = 0, ks = 0;
-    const int t3 = 2 * n_kt;
+    const int t3 = PV_PASS * n_kt;
     const int nloads = npass * n_kt;
     for (int t = 0; t < nloads; ++t) {
       bwait(k_empty + ks, ((kph >> ks) & 1u) ^ 1u, p.xflags & 16);
@@ -321,7 +324,7 @@ __global__ void __launch_bounds__(Cfg<DP>::NTHREADS, 1)
     uint32_t kph = 0;            // per-stage K phase bits
     uint32_t used = 0, c_s = 0;  // per-buffer occupied bit / s_free phase
     int w = 0, n = 0, ks = 0;
-    const int t3 = 2 * n_kt;
+    const int t3 = PV_PASS * n_kt;
     const int nmma = npass * n_kt;
     for (int t = 0; t < nmma; ++t) {
       long long t0 = clk64();
@@ -417,6 +420,12 @@ __global__ void __launch_bounds__(Cfg<DP>::NTHREADS, 1)
     // ---- pass 1: row max over unmasked keys (softmax.py:139-143, :174-179); the row
     // min rides along (free: pass 1 waits on the MMA) to size the unclipped index range
     int32_t mx = INT_MIN, mn = INT_MAX;
+    // QO: running max (real units) and sum of exp(real - qm); real = f32(a) * alpha in f32
+    // as the reference (pipeline.py:277-279); f32(a) * alpha is monotone in a, so the
+    // chunk max is taken on the integers.
+    const float alpha = QO ? (float)((double)hp.s_q * (double)hp.s_k / sqrt((double)p.d)) : 0.0f;
+    constexpr float L2E = 1.4426950408889634f;
+    float qm = -INFINITY, qs = 0.0f;
     for (int n = wg; n < n_kt; n += NWG) {
       long long tw0 = clk64();
       bwait(s_full + wg, s_ph, p.xflags & 4);
@@ -447,7 +456,32 @@ __global__ void __launch_bounds__(Cfg<DP>::NTHREADS, 1)
         // excluded (cut <= 0: whole batch; invalid rows: cut = 0).  Dense masks take
         // the bitmask path.
         const int cut = row_valid ? lim - j0 + 1 : 0;
-        if (p.xflags & 32) {  // experiment: no pass-1 arithmetic
+        if (QO) {
+          const uint32_t ma = p.mask_bits ? (row_valid ? chunk_mask(p, i, j0, lim) : ~0u)
+                                          : (cut >= 32 ? 0u : (cut <= 0 ? ~0u : (0xffffffffu << cut)));
+          const uint32_t mbb = p.mask_bits ? (row_valid ? chunk_mask(p, i, j0 + 32, lim) : ~0u)
+                                           : (cut >= 64 ? 0u : (cut <= 32 ? ~0u : (0xffffffffu << (cut - 32))));
+          int32_t cmx = INT_MIN;
+#pragma unroll
+          for (int e = 0; e < 32; ++e) {
+            if (!((ma >> e) & 1u)) cmx = max(cmx, (int32_t)va[e]);
+            if (!((mbb >> e) & 1u)) cmx = max(cmx, (int32_t)vb[e]);
+          }
+          if (cmx != INT_MIN) {
+            const float cm = __fmul_rn(__int2float_rn(cmx), alpha);
+            if (cm > qm) { qs *= ex2_approx(__fmul_rn(qm - cm, L2E)); qm = cm; }
+            const float mL = qm * L2E;
+            float acc0 = 0.0f, acc1 = 0.0f;
+#pragma unroll
+            for (int e = 0; e < 32; ++e) {
+              const float xa = ex2_approx(fmaf(__fmul_rn(__int2float_rn((int32_t)va[e]), alpha), L2E, -mL));
+              const float xb = ex2_approx(fmaf(__fmul_rn(__int2float_rn((int32_t)vb[e]), alpha), L2E, -mL));
+              acc0 += ((ma >> e) & 1u) ? 0.0f : xa;
+              acc1 += ((mbb >> e) & 1u) ? 0.0f : xb;
+            }
+            qs += acc0 + acc1;
+          }
+        } else if (p.xflags & 32) {  // experiment: no pass-1 arithmetic
         } else if (!p.mask_bits) {
           if (!__any_sync(0xffffffffu, cut < 64)) {
 #pragma unroll
@@ -475,17 +509,40 @@ __global__ void __launch_bounds__(Cfg<DP>::NTHREADS, 1)
       }
     }
     if (tm) IA_TMARK(1);
-    xmax[wg * 128 + row] = mx;
-    xmin[wg * 128 + row] = mn;
-    named_bar_sync(1, NWT);
-    int32_t m = xmax[row];
-    mn = xmin[row];
-#pragma unroll
-    for (int w = 1; w < NWG; ++w) {
-      m = max(m, xmax[w * 128 + row]);
-      mn = min(mn, xmin[w * 128 + row]);
+    if (QO) {
+      xmax[wg * 128 + row] = __float_as_int(qm);
+      xsum[wg * 128 + row] = __float_as_uint(qs);
+    } else {
+      xmax[wg * 128 + row] = mx;
+      xmin[wg * 128 + row] = mn;
     }
-    const bool dead = (m == INT_MIN);  // fully masked row: all-zero P^ (softmax.py:181-184)
+    named_bar_sync(1, NWT);
+    int32_t m = 0;
+    float q_ksc = 0.0f, q_mL = 0.0f;  // QO: p_scale / sum, rowmax * log2(e)
+    bool dead;
+    if (QO) {
+      float M = -INFINITY, Ssum = 0.0f;
+#pragma unroll
+      for (int w = 0; w < NWG; ++w) M = fmaxf(M, __int_as_float(xmax[w * 128 + row]));
+#pragma unroll
+      for (int w = 0; w < NWG; ++w) {
+        const float mw = __int_as_float(xmax[w * 128 + row]);
+        if (mw != -INFINITY) Ssum += __uint_as_float(xsum[w * 128 + row]) * ex2_approx(__fmul_rn(mw - M, L2E));
+      }
+      dead = !(M > -INFINITY) || !(Ssum > 0.0f);  // fully masked row -> zeros (pipeline.py:122-127)
+      q_ksc = dead ? 0.0f : (float)p.scale_x2 * 0.5f / Ssum;
+      q_mL = dead ? 0.0f : M * L2E;
+      named_bar_sync(1, NWT);  // xsum is reused below
+    } else {
+      m = xmax[row];
+      mn = xmin[row];
+#pragma unroll
+      for (int w = 1; w < NWG; ++w) {
+        m = max(m, xmax[w * 128 + row]);
+        mn = min(mn, xmin[w * 128 + row]);
+      }
+      dead = (m == INT_MIN);  // fully masked row: all-zero P^ (softmax.py:181-184)
+    }
     if (dead) m = 0;
     const bool fast = hp.use32 != 0;
     IdxMap im;
@@ -504,7 +561,7 @@ __global__ void __launch_bounds__(Cfg<DP>::NTHREADS, 1)
 
     // ---- pass 2: idx, e = lut[idx], S = sum e (softmax.py:144-155)
     uint32_t S = 0;
-    for (int n = wg; n < n_kt_b; n += NWG) {
+    for (int n = wg; n < (QO ? 0 : n_kt_b); n += NWG) {
       if (!resident) {
         long long tw0 = clk64();
         bwait(s_full + wg, s_ph, p.xflags & 4);
@@ -559,6 +616,7 @@ __global__ void __launch_bounds__(Cfg<DP>::NTHREADS, 1)
       }
     }
     if (tm) IA_TMARK(2);
+    if (!QO) {
     xsum[wg * 128 + row] = S;
     named_bar_sync(1, NWT);
     S = xsum[row];
@@ -574,6 +632,7 @@ __global__ void __launch_bounds__(Cfg<DP>::NTHREADS, 1)
       }
     }
     named_bar_sync(1, NWT);
+    }
     // entry idx of this row: wide: tab_row + idx * 512 (u32), else tab_row + idx * 128 (u8)
     const uint32_t tab_row = smem_u32(tab) + (uint32_t)row * (wtab ? 4u : 1u);
     const uint32_t tab_sh = wtab ? 9u : 7u;
@@ -618,6 +677,23 @@ __global__ void __launch_bounds__(Cfg<DP>::NTHREADS, 1)
         for (int q = 0; q < 16; ++q) pk[q] = 0u;
         const int cut = (row_valid && !dead) ? lim - j0 + 1 : 0;
         if (SKEL) {
+        } else if (QO) {
+          // p^ = floor(exp(real - max) * (scale / sum) + 0.5) (pipeline.py:130-140, 281)
+          if (row_valid && !dead) {
+            const uint32_t ma = p.mask_bits ? chunk_mask(p, i, j0, lim)
+                                            : (cut >= 32 ? 0u : (cut <= 0 ? ~0u : (0xffffffffu << cut)));
+            const uint32_t mbb = p.mask_bits ? chunk_mask(p, i, j0 + 32, lim)
+                                             : (cut >= 64 ? 0u : (cut <= 32 ? ~0u : (0xffffffffu << (cut - 32))));
+#pragma unroll
+            for (int e = 0; e < 32; ++e) {
+              const float xa = ex2_approx(fmaf(__fmul_rn(__int2float_rn((int32_t)va[e]), alpha), L2E, -q_mL));
+              const float xb = ex2_approx(fmaf(__fmul_rn(__int2float_rn((int32_t)vb[e]), alpha), L2E, -q_mL));
+              const uint32_t ba = ((ma >> e) & 1u) ? 0u : min(__float2uint_rz(fmaf(xa, q_ksc, 0.5f)), 255u);
+              const uint32_t bb = ((mbb >> e) & 1u) ? 0u : min(__float2uint_rz(fmaf(xb, q_ksc, 0.5f)), 255u);
+              pk[e >> 2] |= ba << (8 * (e & 3));
+              pk[8 + (e >> 2)] |= bb << (8 * (e & 3));
+            }
+          }
         } else if (!p.mask_bits && fast && wtab) {
           const bool any_cut = __any_sync(0xffffffffu, cut < 64);
           if (uncl3 && !any_cut) {
@@ -765,7 +841,7 @@ bool attn_supported(int nlut) {
   return attn_smem_bytes<DP>(nlut) + 256 <= 227 * 1024;
 }
 
-template <int DP, bool DEBUG, bool SKEL = false>
+template <int DP, bool DEBUG, bool SKEL = false, bool QO = false>
 static int launch_attn(const ia_attn_args* a, cudaStream_t st) {
   using C = Cfg<DP>;
   if (!attn_supported<DP>(a->nlut))
@@ -807,7 +883,7 @@ static int launch_attn(const ia_attn_args* a, cudaStream_t st) {
   for (int t = 0; t < 256; ++t) dv.lut[t] = t < a->nlut ? a->lut[t] : 0;
   size_t smem = attn_smem_bytes<DP>(a->nlut);
   if (smem < 120 * 1024) smem = 120 * 1024;  // one CTA per SM (it owns all 512 TMEM columns)
-  auto kern = attn_fwd_kernel<DP, DEBUG, SKEL>;
+  auto kern = attn_fwd_kernel<DP, DEBUG, SKEL, QO>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return fail(IA_ERR_CUDA, "smem attribute: %s", cudaGetErrorString(e));
   const uint64_t grid = (uint64_t)dv.n_qt * BH;
@@ -851,6 +927,16 @@ extern "C" int ia_attn_fwd(const ia_attn_args* a, void* stream) {
     return fail(IA_ERR_INVALID_ARGUMENT, "operands must be 16-byte aligned");
   cudaStream_t st = (cudaStream_t)stream;
   const bool dbg = a->dbg_logits || a->dbg_prob || a->dbg_acc;
+  if (a->softmax_mode == IA_SOFTMAX_FLOAT) {  // quant-only comparator
+    switch (a->d_pad) {
+      case 32: return dbg ? launch_attn<32, true, false, true>(a, st) : launch_attn<32, false, false, true>(a, st);
+      case 64: return dbg ? launch_attn<64, true, false, true>(a, st) : launch_attn<64, false, false, true>(a, st);
+      case 128: return dbg ? launch_attn<128, true, false, true>(a, st) : launch_attn<128, false, false, true>(a, st);
+      default: return dbg ? launch_attn<256, true, false, true>(a, st) : launch_attn<256, false, false, true>(a, st);
+    }
+  }
+  if (a->softmax_mode != IA_SOFTMAX_INDEX)
+    return fail(IA_ERR_INVALID_ARGUMENT, "ia_attn_fwd: unknown softmax_mode %d", a->softmax_mode);
   switch (a->d_pad) {
     case 32: return dbg ? launch_attn<32, true>(a, st) : launch_attn<32, false>(a, st);
     case 64: return dbg ? launch_attn<64, true>(a, st) : launch_attn<64, false>(a, st);

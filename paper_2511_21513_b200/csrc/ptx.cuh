@@ -290,4 +290,12 @@ __device__ __forceinline__ uint32_t warp_id() {
   return __shfl_sync(0xffffffffu, threadIdx.x >> 5, 0);
 }
 
+
+// 2^x, MUFU.EX2 (approximate; the quant-only comparator's exp, as FlashAttention-style
+// kernels compute it)
+__device__ __forceinline__ float ex2_approx(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
 }  // namespace ia

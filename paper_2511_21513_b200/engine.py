@@ -211,7 +211,7 @@ def _finish_prepare(qhat, khat, vt, sq, sk, sv, ws, per_head, B, H, Hkv, d, b, c
 
 
 def attn_fused(prep: Prepared, shape, out, *, causal=False, seq_lens=None, mask_bits=None,
-               lut=None, p_scale=255, debug=None, times=None):
+               lut=None, p_scale=255, debug=None, times=None, softmax_mode=_lib.IA_SOFTMAX_INDEX):
     B, H, Hkv, Lq, d = shape
     a = _lib.AttnArgs()
     a.q, a.k, a.vt = prep.qhat.data_ptr(), prep.khat.data_ptr(), prep.vt.data_ptr()
@@ -223,6 +223,7 @@ def attn_fused(prep: Prepared, shape, out, *, causal=False, seq_lens=None, mask_
     a.causal = int(bool(causal))
     a.nlut = len(lut)
     a.p_scale = int(p_scale)
+    a.softmax_mode = int(softmax_mode)
     for i, x in enumerate(lut):
         a.lut[i] = int(x)
     if debug is not None:
@@ -246,8 +247,12 @@ def lut_bytes(b: int, c: float) -> np.ndarray:
 
 def attention(q, k, v, *, causal=False, seq_lens=None, mask=None, scale_granularity="head",
               b=5, c=6.6, p_scale=255, lut=None, out=None, debug=False, check_finite=True,
-              timer=None, scales=None):
+              timer=None, scales=None, softmax="index"):
     """Batched fused IntAttention on the current CUDA device.
+
+    softmax="index" is IndexSoftmax (bit-exact with the reference); "float" runs
+    the quant-only comparator (pipeline.py:259-296: dequantise -> f32 softmax ->
+    requantise between the same INT8 MMAs) in the same fused kernel.
 
     q [B, H, L, d], k/v [B, Hkv, L, d]: f32 CUDA tensors (contiguous).
     seq_lens: int32 CUDA [B] or None.  mask: bool CUDA [L, L] (True = excluded)
@@ -266,6 +271,10 @@ def attention(q, k, v, *, causal=False, seq_lens=None, mask=None, scale_granular
     d_pad = pad_head_dim(d)
     if d_pad is not None and _lib.load().ia_attn_supported(d_pad, len(lut)) != _lib.IA_OK:
         d_pad = None  # e.g. d_pad 256 with a 2^6+ entry LUT: shared memory too small
+    if softmax not in ("index", "float"):
+        raise ValueError("softmax must be 'index' or 'float'")
+    if d_pad is None and softmax == "float":
+        raise ValueError("the fused quant-only path needs head dim <= 256")
     if d_pad is None:
         if scales is not None:
             raise ValueError("precomputed scales need the fused path (head dim <= 256)")
@@ -287,7 +296,8 @@ def attention(q, k, v, *, causal=False, seq_lens=None, mask=None, scale_granular
                "prob": torch.zeros((B * H, Lq, Lq), dtype=torch.uint8, device=q.device),
                "acc": torch.zeros((B * H, Lq, d_pad), dtype=torch.int32, device=q.device)}
     attn_fused(prep, (B, H, Hkv, Lq, d), out, causal=causal, seq_lens=seq_lens,
-               mask_bits=mbits, lut=lut, p_scale=p_scale, debug=dbg)
+               mask_bits=mbits, lut=lut, p_scale=p_scale, debug=dbg,
+               softmax_mode=_lib.IA_SOFTMAX_FLOAT if softmax == "float" else _lib.IA_SOFTMAX_INDEX)
     if timer is not None:
         timer.mark("attention")
     if isinstance(check_finite, list):  # deferred: the caller checks after its pipeline

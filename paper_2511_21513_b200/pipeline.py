@@ -226,9 +226,11 @@ def _quantize_probs(p, p_format):
 
 def quant_only_attention(q, k, v, cfg=None, warmup=0, iters=1):
     """The paper's comparator: INT8 GEMMs with a dequantise -> f32 softmax ->
-    requantise detour (pipeline.py:259-296).  The GEMMs are the library's
-    tcgen05 kernels; the float softmax is torch on the device, so results match
-    the reference to float tolerance (device expf), not bit for bit."""
+    requantise detour (pipeline.py:259-296).  Per-tensor K with d <= 256 runs the
+    fused kernel's quant-only mode (MUFU exp2 between the same tcgen05 INT8
+    MMAs); per-row-group K composes the library's tcgen05 GEMMs with a torch f32
+    softmax.  Either way results match the reference to float tolerance, not bit
+    for bit."""
     from .gemm import gemm_pv, matmul_int8
     from .quantize import quantize_symmetric
 
@@ -239,6 +241,18 @@ def quant_only_attention(q, k, v, cfg=None, warmup=0, iters=1):
     numpy_in = not is_torch(q)
     qt, kt, vt = (to_device(x, np.float32) for x in (q, k, v))
     mt = to_device(mask).to(torch.bool) if mask is not None else None
+
+    if k_gran.kind == PER_TENSOR and E.pad_head_dim(d) is not None:
+        # fused kernel, quant-only mode (IA_SOFTMAX_FLOAT): same quantiser and MMAs
+        def fused(clk):
+            return E.attention(qt[None, None], kt[None, None], vt[None, None], mask=mt,
+                               p_scale=cfg.p_format.value, timer=clk, softmax="float")
+
+        out, timings = _run_measured(
+            fused, warmup, iters,
+            {"quantize": ("start", "quantized"), "softmax_path": ("quantized", "attention"),
+             "total": ("start", "attention")})
+        return to_host(out[0, 0], numpy_in), timings
 
     def once(clk):
         if clk:

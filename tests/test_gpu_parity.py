@@ -299,3 +299,60 @@ def test_grouped_pipeline_golden():
                                  mask=mask)
         out, _ = ia.int_attention(G[key + "_q"], G[key + "_k"], G[key + "_v"], cfg)
         assert np.array_equal(np.asarray(out).view(np.uint32), G[key + "_out"].view(np.uint32)), key
+
+
+def _qo_gold():
+    import os
+    return np.load(os.path.join(os.path.dirname(__file__), "golden", "quant_only_cases.npz"))
+
+
+@pytest.mark.parametrize("i", range(5))
+def test_quant_only_fused_vs_reference(i):
+    """Fused quant-only mode (IA_SOFTMAX_FLOAT) vs the reference's quant_only_attention.
+
+    Tolerance (float comparator, MUFU exp2 vs numpy f32 exp): every requantised P^
+    within 1 of the reference's and at most 1% of entries off; each output element
+    within n_i * 127 * s_v / denom of the reference, n_i = the row's P^ mismatches
+    (a P^ unit moves one output by at most |v^| <= 127 grid steps)."""
+    G = _qo_gold()
+    key = f"qo{i}"
+    q, k, v = G[key + "_q"], G[key + "_k"], G[key + "_v"]
+    mask = G[key + "_mask"]
+    mask = None if mask.size == 0 else mask
+    pfv = int(G[key + "_pf"])
+    cfg = ia.AttentionConfig(p_format=ia.PFormat.UINT8X255 if pfv == 255 else ia.PFormat.INT8X127)
+    out, dbg = ia.quant_only_attention_batched(q[None, None], k[None, None], v[None, None],
+                                               mask=mask, cfg=cfg, debug=True)
+    L = q.shape[0]
+    ph = dbg["prob"][0].cpu().numpy().astype(np.int32)
+    want = G[key + "_phat"].astype(np.int32)
+    diff = np.abs(ph - want)
+    assert diff.max() <= 1, f"P^ off by {diff.max()}"
+    assert (diff > 0).mean() <= 0.01, f"{(diff > 0).mean():.4f} of P^ entries differ"
+    n_i = (diff > 0).sum(axis=1)
+    bound = n_i[:, None] * 127.0 * float(G[key + "_sv"]) / pfv + 1e-6
+    err = np.abs(out[0, 0] - G[key + "_out"])
+    assert (err <= bound).all(), float((err - bound).max())
+    # the single-head API takes the same fused path
+    o1, _ = ia.quant_only_attention(q, k, v, ia.AttentionConfig(mask=mask, p_format=cfg.p_format))
+    assert np.array_equal(o1.view(np.uint32), out[0, 0].view(np.uint32))
+    if mask is not None and mask.all(axis=1).any():
+        assert not out[0, 0][mask.all(axis=1)].view(np.uint32).any()  # fully masked rows -> +0.0
+
+
+def test_quant_only_fused_batched_gqa_causal():
+    """Batched GQA / varlen quant-only mode: each unit equals its single-head run."""
+    rng = np.random.default_rng(5)
+    B, H, Hkv, L, d = 2, 4, 2, 700, 64
+    q = rng.standard_normal((B, H, L, d), dtype=np.float32)
+    k = rng.standard_normal((B, Hkv, L, d), dtype=np.float32)
+    v = rng.standard_normal((B, Hkv, L, d), dtype=np.float32)
+    lens = np.array([700, 450], np.int32)
+    out = ia.quant_only_attention_batched(q, k, v, causal=True, seq_lens=lens)
+    for b in range(B):
+        n = int(lens[b])
+        for h in range(H):
+            o1, _ = ia.quant_only_attention(q[b, h, :n], k[b, h // 2, :n], v[b, h // 2, :n],
+                                            ia.AttentionConfig(mask=np.triu(np.ones((n, n), bool), 1)))
+            assert np.array_equal(out[b, h, :n].view(np.uint32), o1.view(np.uint32)), (b, h)
+            assert not out[b, h, n:].view(np.uint32).any()
