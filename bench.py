@@ -343,6 +343,25 @@ def run_gpu(args, wl_name):
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         e2e_t = float(tt.item())
 
+    # ---- the paper's comparator on the same inputs: quant-only mode of the fused
+    # kernel (dequantise -> f32 softmax -> requantise between the same INT8 MMAs)
+    qo_ms = None
+    if rank == 0 and not args.no_comparator:
+        def qo_step():
+            E.attention(q, k, v, causal=wl.causal, seq_lens=sl, scale_granularity=gran, lut=lut,
+                        out=out, check_finite=False, softmax="float")
+        for _ in range(2):
+            qo_step()
+        c0 = torch.cuda.Event(enable_timing=True)
+        c1 = torch.cuda.Event(enable_timing=True)
+        n_qo = max(3, min(args.steps, 10))
+        c0.record()
+        for _ in range(n_qo):
+            qo_step()
+        c1.record()
+        torch.cuda.synchronize()
+        qo_ms = c0.elapsed_time(c1) / n_qo
+
     ops = wl.ops()
     tokens = wl.tokens()
     step_s = elapsed / args.steps
@@ -392,9 +411,16 @@ def run_gpu(args, wl_name):
                     "d2h_bytes_per_step": 4 * wl.q.size,
                     "path": "int_attention_batched(pinned host f32 in, pinned host f32 out; "
                             "chunked H2D / kernel / D2H overlap inside the call)"},
-            "gpu_launches": 9 * args.steps,
+            # per step: ia_quant_heads + head_params + attn_fwd (the workspace memset is torch's)
+            "gpu_launches": 3 * args.steps,
             "clocks": clk.summary(),
         }
+        if qo_ms is not None:
+            line["comparator"] = {
+                "pipeline": "quant_only (pipeline.py:259-296) as the fused kernel's "
+                            "IA_SOFTMAX_FLOAT mode, same quantiser and MMAs",
+                "ms_per_step": qo_ms, "tops": ops / (qo_ms / 1e3) / 1e12,
+                "int_attention_speedup": qo_ms / (1e3 * step_s)}
         if cb is not None:
             line["cpu_baseline"] = {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")}
         print(json.dumps(line))
@@ -412,6 +438,8 @@ def main():
     ap.add_argument("--workload", default="C4", choices=["C1", "C2", "C3", "C4", "C5"])
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-comparator", action="store_true",
+                    help="skip timing the quant-only comparator mode")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
