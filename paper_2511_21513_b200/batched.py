@@ -97,9 +97,11 @@ def _pinned(x):
 
 def _host_pipelined(q, k, v, *, causal, seq_lens, mask, cfg, out, check_finite, numpy_in):
     """Host-resident inputs with per-head scales: stream the problem through the
-    device in (batch, KV-head group) chunks so the host->device copy of chunk
-    i+1, the fused kernel on chunk i and the device->host copy of chunk i-1
-    overlap (three CUDA streams, two device buffer slots).  Per-head scales and
+    device in (batch, KV-head group) chunks -- split into two query-head halves
+    sharing the group's K/V when a chunk is a single GQA group -- so the
+    host->device copy of chunk i+1, the fused kernel on chunk i and the
+    device->host copy of chunk i-1 overlap (three CUDA streams, two device buffer
+    slots).  Per-head scales and
     per-unit outputs depend only on the unit's own data, so every chunk's result
     is bit-identical to the one-shot launch."""
     dev = E.require_device()
@@ -117,60 +119,83 @@ def _host_pipelined(q, k, v, *, causal, seq_lens, mask, cfg, out, check_finite, 
         mt = to_device(mask).to(torch.bool)
         if tuple(mt.shape) != (L, L):
             raise ValueError(f"mask must be {L}x{L}, got {tuple(mt.shape)}")
-    # ~8+ chunks of whole KV groups (at least one KV head each)
+    # ~8+ chunks of whole KV groups (at least one KV head each).  With one KV head per
+    # chunk and GQA, each group is sent as two sub-chunks (K, V + the first half of its
+    # query heads, then the second half reusing the K/V already on the device): halves
+    # the pipeline fill (first H2D) and drain (last kernel + D2H) at no extra PCIe bytes.
     unit_bytes = 4 * L * d * (G + 2)
     per = max(1, min(Hkv, (B * Hkv * unit_bytes // 8) // unit_bytes))
-    chunks = [(b, j, min(j + per, Hkv)) for b in range(B) for j in range(0, Hkv, per)]
+    chunks = []  # (b, kv j0, kv j1, q head lo, q head hi, sends K/V)
+    for b in range(B):
+        for j in range(0, Hkv, per):
+            j1 = min(j + per, Hkv)
+            if j1 - j == 1 and G >= 2:
+                chunks.append((b, j, j1, j * G, j * G + G // 2, True))
+                chunks.append((b, j, j1, j * G + G // 2, j1 * G, False))
+            else:
+                chunks.append((b, j, j1, j * G, j1 * G, True))
     if out is not None and is_torch(out) and out.device.type == "cpu":
         oh = out
     else:
         oh = torch.empty((B, H, L, d), dtype=torch.float32, pin_memory=True)
+    # Q / O buffers double-buffered per chunk, K / V double-buffered per KV group (a
+    # group's second half reads the K / V its first half brought in)
     slots = [{"q": torch.empty((1, per * G, L, d), dtype=torch.float32, device=dev),
-              "k": torch.empty((1, per, L, d), dtype=torch.float32, device=dev),
-              "v": torch.empty((1, per, L, d), dtype=torch.float32, device=dev),
               "o": torch.empty((1, per * G, L, d), dtype=torch.float32, device=dev)}
+             for _ in range(2)]
+    kvbuf = [{"k": torch.empty((1, per, L, d), dtype=torch.float32, device=dev),
+              "v": torch.empty((1, per, L, d), dtype=torch.float32, device=dev)}
              for _ in range(2)]
     sl_d = None if sl_h is None else torch.as_tensor(sl_h.astype(np.int32)).to(dev)
     main = torch.cuda.current_stream()
     s_in, s_run, s_out = torch.cuda.Stream(), torch.cuda.Stream(), torch.cuda.Stream()
     for s in (s_in, s_run, s_out):
         s.wait_stream(main)
-    ran = [None, None]   # compute of the chunk that last used the slot (inputs free after)
+    q_read = [None, None]   # last compute that read the slot's Q
+    kv_read = [None, None]  # last compute that read the K / V buffer
     drained = [None, None]  # device->host copy that last read the slot's output
     errs = [] if check_finite else False
-    for i, (b, j0, j1) in enumerate(chunks):
-        sl = slots[i % 2]
-        nh = j1 - j0
-        qs, ks_, vs, os_ = (sl["q"][:, :nh * G], sl["k"][:, :nh], sl["v"][:, :nh],
-                            sl["o"][:, :nh * G])
+    grp = -1
+    for i, (b, j0, j1, qa, qb, send_kv) in enumerate(chunks):
+        si = i % 2
+        sl = slots[si]
+        if send_kv:
+            grp += 1
+        kb = kvbuf[grp % 2]
+        nkv, nq = j1 - j0, qb - qa
+        qs, os_ = sl["q"][:, :nq], sl["o"][:, :nq]
+        ks_, vs = kb["k"][:, :nkv], kb["v"][:, :nkv]
         with torch.cuda.stream(s_in):
-            if ran[i % 2] is not None:
-                s_in.wait_event(ran[i % 2])
-            qs.copy_(qh[b:b + 1, j0 * G:j1 * G], non_blocking=True)
-            ks_.copy_(kh[b:b + 1, j0:j1], non_blocking=True)
-            vs.copy_(vh[b:b + 1, j0:j1], non_blocking=True)
+            if send_kv:
+                if kv_read[grp % 2] is not None:
+                    s_in.wait_event(kv_read[grp % 2])
+                ks_.copy_(kh[b:b + 1, j0:j1], non_blocking=True)
+                vs.copy_(vh[b:b + 1, j0:j1], non_blocking=True)
+            if q_read[si] is not None:
+                s_in.wait_event(q_read[si])
+            qs.copy_(qh[b:b + 1, qa:qb], non_blocking=True)
             loaded = torch.cuda.Event()
             loaded.record(s_in)
         with torch.cuda.stream(s_run):
             s_run.wait_event(loaded)
-            if drained[i % 2] is not None:
-                s_run.wait_event(drained[i % 2])
+            if drained[si] is not None:
+                s_run.wait_event(drained[si])
             E.attention(qs, ks_, vs, causal=causal,
                         seq_lens=None if sl_d is None else sl_d[b:b + 1], mask=mt,
                         scale_granularity="head", b=cfg.b, c=cfg.c,
                         p_scale=cfg.p_format.value, out=os_, check_finite=errs)
             done = torch.cuda.Event()
             done.record(s_run)
-            ran[i % 2] = done
+            q_read[si] = done
+            kv_read[grp % 2] = done
         with torch.cuda.stream(s_out):
             s_out.wait_event(done)
-            oh[b:b + 1, j0 * G:j1 * G].copy_(os_, non_blocking=True)
+            oh[b:b + 1, qa:qb].copy_(os_, non_blocking=True)
             ev = torch.cuda.Event()
             ev.record(s_out)
-            drained[i % 2] = ev
+            drained[si] = ev
     s_out.synchronize()
     main.wait_stream(s_run)
-    if errs:
-        for e in errs:
-            E.raise_if_nonfinite(e)
+    if errs:  # one host sync for every chunk's non-finite flag
+        E.raise_if_nonfinite(torch.stack(errs).amax())
     return oh.numpy() if numpy_in else oh
