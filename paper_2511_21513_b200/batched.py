@@ -155,29 +155,41 @@ def _host_pipelined(q, k, v, *, causal, seq_lens, mask, cfg, out, check_finite, 
     kv_read = [None, None]  # last compute that read the K / V buffer
     drained = [None, None]  # device->host copy that last read the slot's output
     errs = [] if check_finite else False
-    grp = -1
-    for i, (b, j0, j1, qa, qb, send_kv) in enumerate(chunks):
-        si = i % 2
-        sl = slots[si]
-        if send_kv:
-            grp += 1
-        kb = kvbuf[grp % 2]
-        nkv, nq = j1 - j0, qb - qa
-        qs, os_ = sl["q"][:, :nq], sl["o"][:, :nq]
-        ks_, vs = kb["k"][:, :nkv], kb["v"][:, :nkv]
+    # K / V buffer of every chunk (a new group starts at each chunk that sends K / V)
+    kv_of, g = [], -1
+    for c in chunks:
+        g += 1 if c[5] else 0
+        kv_of.append(g % 2)
+    loaded = [None] * len(chunks)
+
+    def h2d(i):
+        b, j0, j1, qa, qb, send_kv = chunks[i]
+        si, kb = i % 2, kvbuf[kv_of[i]]
         with torch.cuda.stream(s_in):
             if send_kv:
-                if kv_read[grp % 2] is not None:
-                    s_in.wait_event(kv_read[grp % 2])
-                ks_.copy_(kh[b:b + 1, j0:j1], non_blocking=True)
-                vs.copy_(vh[b:b + 1, j0:j1], non_blocking=True)
+                if kv_read[kv_of[i]] is not None:
+                    s_in.wait_event(kv_read[kv_of[i]])
+                kb["k"][:, :j1 - j0].copy_(kh[b:b + 1, j0:j1], non_blocking=True)
+                kb["v"][:, :j1 - j0].copy_(vh[b:b + 1, j0:j1], non_blocking=True)
             if q_read[si] is not None:
                 s_in.wait_event(q_read[si])
-            qs.copy_(qh[b:b + 1, qa:qb], non_blocking=True)
-            loaded = torch.cuda.Event()
-            loaded.record(s_in)
+            slots[si]["q"][:, :qb - qa].copy_(qh[b:b + 1, qa:qb], non_blocking=True)
+            loaded[i] = torch.cuda.Event()
+            loaded[i].record(s_in)
+
+    # enqueue order H2D(i+1), kernel(i), D2H(i): the host never holds back the next
+    # chunk's copy behind this chunk's launch overhead
+    h2d(0)
+    for i, (b, j0, j1, qa, qb, send_kv) in enumerate(chunks):
+        if i + 1 < len(chunks):
+            h2d(i + 1)
+        si = i % 2
+        nkv, nq = j1 - j0, qb - qa
+        qs, os_ = slots[si]["q"][:, :nq], slots[si]["o"][:, :nq]
+        kb = kvbuf[kv_of[i]]
+        ks_, vs = kb["k"][:, :nkv], kb["v"][:, :nkv]
         with torch.cuda.stream(s_run):
-            s_run.wait_event(loaded)
+            s_run.wait_event(loaded[i])
             if drained[si] is not None:
                 s_run.wait_event(drained[si])
             E.attention(qs, ks_, vs, causal=causal,
@@ -187,7 +199,7 @@ def _host_pipelined(q, k, v, *, causal, seq_lens, mask, cfg, out, check_finite, 
             done = torch.cuda.Event()
             done.record(s_run)
             q_read[si] = done
-            kv_read[grp % 2] = done
+            kv_read[kv_of[i]] = done
         with torch.cuda.stream(s_out):
             s_out.wait_event(done)
             oh[b:b + 1, qa:qb].copy_(os_, non_blocking=True)
