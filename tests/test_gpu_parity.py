@@ -356,3 +356,56 @@ def test_quant_only_fused_batched_gqa_causal():
                                             ia.AttentionConfig(mask=np.triu(np.ones((n, n), bool), 1)))
             assert np.array_equal(out[b, h, :n].view(np.uint32), o1.view(np.uint32)), (b, h)
             assert not out[b, h, n:].view(np.uint32).any()
+
+
+def _fuzz_case(i):
+    """Seeded random batched problem: shapes, GQA ratio, masks, lengths, LUT bits, clip
+    bound, P format, scale granularity, input magnitudes and outlier channels."""
+    rng = np.random.default_rng(10_000 + i)
+    B = int(rng.integers(1, 4))
+    Hkv = int(rng.integers(1, 4))
+    H = Hkv * int(rng.choice([1, 2, 4]))
+    L = int(rng.integers(1, 700))
+    d = int(rng.choice([int(rng.integers(1, 257)), 32, 64, 128, 256, int(rng.integers(257, 301))],
+                       p=[0.4, 0.1, 0.15, 0.15, 0.1, 0.1]))
+    causal = bool(rng.integers(0, 2))
+    lens = None
+    if rng.random() < 0.5:
+        lens = rng.integers(0, L + 1, size=B).astype(np.int32)
+        lens[0] = L if rng.random() < 0.5 else lens[0]
+    gran = "tensor" if rng.random() < 0.3 else "head"
+    cfg = ia.AttentionConfig(b=int(rng.choice([3, 4, 5, 6])), c=float(rng.choice([4.4, 6.6, 8.8])),
+                             p_format=ia.PFormat.INT8X127 if rng.random() < 0.3 else ia.PFormat.UINT8X255)
+    mags = [np.float32(10.0 ** rng.uniform(-2, 2)) for _ in range(3)]
+    q = rng.standard_normal((B, H, L, d), dtype=np.float32) * mags[0]
+    k = rng.standard_normal((B, Hkv, L, d), dtype=np.float32) * mags[1]
+    v = rng.standard_normal((B, Hkv, L, d), dtype=np.float32) * mags[2]
+    if rng.random() < 0.3:  # outlier channels
+        ch = rng.choice(d, size=max(1, d // 50), replace=False)
+        q[..., ch] *= np.float32(10.0)
+        k[..., ch] *= np.float32(10.0)
+    if lens is not None:
+        for b, n in enumerate(lens):
+            q[b, :, n:] = 0
+            k[b, :, n:] = 0
+            v[b, :, n:] = 0
+    return q, k, v, causal, lens, gran, cfg, bool(rng.integers(0, 2))
+
+
+@pytest.mark.parametrize("i", range(120))
+def test_fuzz_batched_vs_oracle(i):
+    """120 seeded random problems through int_attention_batched (host pipeline or
+    device tensors; fused kernel or, for d > 256, the stage kernels), bit-exact
+    against the oracle, which is itself pinned to the live reference."""
+    q, k, v, causal, lens, gran, cfg, on_device = _fuzz_case(i)
+    args = (q, k, v)
+    if on_device:
+        args = tuple(torch.from_numpy(x).cuda() for x in args)
+    got = ia.int_attention_batched(*args, causal=causal, seq_lens=lens, scale_granularity=gran,
+                                   cfg=cfg)
+    if on_device:
+        got = got.cpu().numpy()
+    want, _ = O.attention_batched(q, k, v, causal=causal, seq_lens=lens, scale_granularity=gran,
+                                  b=cfg.b, c=cfg.c, p_scale=cfg.p_format.value)
+    assert np.array_equal(got.view(np.uint32), want.view(np.uint32)), \
+        (q.shape, k.shape, causal, lens, gran, cfg, _first_diff(got, want))
