@@ -53,7 +53,7 @@ struct QHArgs {
 constexpr int QH_THREADS = 512;
 constexpr int QH_TILE_PITCH = 64 + 16;  // transpose tile row pitch (bytes)
 
-__global__ void __launch_bounds__(QH_THREADS) quant_heads_kernel(const QHArgs a) {
+__global__ void __launch_bounds__(QH_THREADS, 3) quant_heads_kernel(const QHArgs a) {
   __shared__ uint32_t red[QH_THREADS / 32];
   __shared__ float s_sh;
   extern __shared__ __align__(16) uint8_t tile[];  // [d_pad][QH_TILE_PITCH] (V^T blocks)
