@@ -409,3 +409,36 @@ def test_fuzz_batched_vs_oracle(i):
                                   b=cfg.b, c=cfg.c, p_scale=cfg.p_format.value)
     assert np.array_equal(got.view(np.uint32), want.view(np.uint32)), \
         (q.shape, k.shape, causal, lens, gran, cfg, _first_diff(got, want))
+
+
+def test_max_sequence_length():
+    """L = MAX_SEQ_LEN (65536, gemm.py:26): the fused kernel's 512 key tiles, ring
+    phases and index maps at the limit, bit-exact vs the oracle on a row sample;
+    one more key is rejected as the reference rejects it."""
+    L, d = 65536, 64
+    rng = np.random.default_rng(65536)
+    q = rng.standard_normal((1, 1, L, d), dtype=np.float32)
+    k = rng.standard_normal((1, 1, L, d), dtype=np.float32)
+    v = rng.standard_normal((1, 1, L, d), dtype=np.float32)
+    got = ia.int_attention_batched(torch.from_numpy(q).cuda(), torch.from_numpy(k).cuda(),
+                                   torch.from_numpy(v).cuda(), causal=True).cpu().numpy()
+    stride = 97
+    want, _ = O.attention_batched(q, k, v, causal=True, row_stride=stride)
+    rows = np.arange(0, L, stride)
+    assert np.array_equal(got[0, 0, rows].view(np.uint32), want[0, 0, rows].view(np.uint32))
+    with pytest.raises(ValueError):
+        ia.int_attention_batched(np.zeros((1, 1, L + 1, 8), np.float32),
+                                 np.zeros((1, 1, L + 1, 8), np.float32),
+                                 np.zeros((1, 1, L + 1, 8), np.float32))
+
+
+def test_single_row_and_single_key():
+    """L = 1 (one query, one key): P^ = 255 on the only key, out = v^ * s_v."""
+    rng = np.random.default_rng(1)
+    for d in (1, 7, 128):
+        q = rng.standard_normal((1, 1), dtype=np.float32).repeat(d, 1)
+        k = rng.standard_normal((1, d), dtype=np.float32)
+        v = rng.standard_normal((1, d), dtype=np.float32)
+        out, _ = ia.int_attention(q, k, v)
+        want = O.int_attention(q, k, v)
+        assert np.array_equal(out.view(np.uint32), want.view(np.uint32))
