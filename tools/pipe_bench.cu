@@ -28,6 +28,7 @@ struct Opt {
   int kst;       // MMA K steps per tile (4 = d 128)
   int cmode;     // consumer: 0 normal; 1 no TMEM loads; 2 spin waits; 3 no tcgen05 fences
   int lean;      // issuer: lane-0-only loop, counters instead of modulo, unrolled K steps
+  int nwg;       // consumer warpgroups (0: = nbuf); WG w takes tiles w, w + nwg, ... (buffer t % nbuf)
 };
 
 __device__ uint64_t g_tr[4][768];  // CTA 0 event clocks: issuer start, issuer issued, consumer woke, consumer freed
@@ -35,21 +36,22 @@ __device__ uint64_t g_tr[4][768];  // CTA 0 event clocks: issuer start, issuer i
 __global__ void __launch_bounds__(544, 1) pipe_kernel(Opt o, uint64_t* res, int* sink) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
-  __shared__ uint64_t bars[8];
+  __shared__ uint64_t bars[16];
   __shared__ uint32_t tslot;
   __shared__ uint8_t lut8[32];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int NB = o.nbuf;
   uint64_t* s_full = bars;
-  uint64_t* s_free = bars + 4;
+  uint64_t* s_free = bars + 8;
+  const int NWGC = o.nwg ? o.nwg : o.nbuf;
   if (threadIdx.x == 0) {
-    for (int i = 0; i < 4; ++i) { mbar_init(s_full + i, 1); mbar_init(s_free + i, 4); }
+    for (int i = 0; i < 8; ++i) { mbar_init(s_full + i, 1); mbar_init(s_free + i, 4); }
     fence_mbar_init();
   }
   if (threadIdx.x < 32) lut8[threadIdx.x] = (uint8_t)(255 >> (threadIdx.x / 4));
   for (int i = threadIdx.x; i < 65536 / 4; i += blockDim.x)
     reinterpret_cast<uint32_t*>(smem)[i] = (i * 2654435761u) & 0x3f3f3f3fu;
-  const int issuer_warp = 4 * NB;
+  const int issuer_warp = 4 * NWGC;
   if (warp == issuer_warp) { tmem_alloc(&tslot, 512); tmem_relinquish(); }
   tc_fence_before();
   __syncthreads();
@@ -119,17 +121,19 @@ __global__ void __launch_bounds__(544, 1) pipe_kernel(Opt o, uint64_t* res, int*
       mbar_wait(s_full, 0);
       if (lane == 0) res[blockIdx.x] = clk() - t0;
     }
-  } else if (warp < 4 * NB && o.mode != 1) {
+  } else if (warp < 4 * NWGC && o.mode != 1) {
     const int wg = warp >> 2, quad = warp & 3;
-    const uint32_t base = tmem + ((uint32_t)(quad * 32) << 16) + wg * bcols;
+    const uint32_t base0 = tmem + ((uint32_t)(quad * 32) << 16);
     int32_t mx = INT_MIN, mn = INT_MAX;
     uint32_t S = 0;
     uint32_t ph = 0;
     const uint32_t M = 0x2468acefu;
-    for (int t = wg; t < T; t += NB) {
-      if (o.cmode == 2) mbar_wait_spin(s_full + wg, ph);
-      else mbar_wait(s_full + wg, ph);
-      ph ^= 1;
+    for (int t = wg; t < T; t += NWGC) {
+      const int bf = t % NB;
+      const uint32_t base = base0 + bf * bcols;
+      if (o.cmode == 2) mbar_wait_spin(s_full + bf, (ph >> bf) & 1u);
+      else mbar_wait(s_full + bf, (ph >> bf) & 1u);
+      ph ^= 1u << bf;
       if (blockIdx.x == 0 && quad == 0 && lane == 0 && t < 768) g_tr[2][t] = clk();
       if (o.cmode != 3) tc_fence_after();
       const int nh = o.ncols / 64;
@@ -144,7 +148,7 @@ __global__ void __launch_bounds__(544, 1) pipe_kernel(Opt o, uint64_t* res, int*
         if ((o.early && hb == 0) || (!o.early && hb == nh - 1)) {
           if (o.cmode != 3) tc_fence_before();
           __syncwarp();
-          if (lane == 0) mbar_arrive(s_free + wg);
+          if (lane == 0) mbar_arrive(s_free + bf);
           if (blockIdx.x == 0 && quad == 0 && lane == 0 && t < 768) g_tr[3][t] = clk();
         }
         if (o.work == 1) {
@@ -178,20 +182,16 @@ int main() {
   cudaMalloc(&d_res, 148 * 8);
   cudaMalloc(&d_sink, 4096 * 4);
   cudaFuncSetAttribute(pipe_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 80 * 1024);
-  struct V { int nbuf, ncols, work, early, spin, mode, kst, cmode, lean; };
+  struct V { int nbuf, ncols, work, early, spin, mode, kst, cmode, lean, nwg; };
   const V vs[] = {
-      {3, 128, 0, 0, 0, 1, 4, 0, 1}, {3, 128, 0, 0, 0, 2, 4, 0, 1}, {3, 128, 0, 0, 0, 0, 4, 0, 1},
-      {3, 128, 1, 0, 0, 0, 4, 0, 1}, {3, 128, 2, 0, 0, 0, 4, 0, 1}, {2, 256, 0, 0, 0, 1, 4, 0, 1},
-      {2, 256, 1, 0, 0, 0, 4, 0, 1}, {4, 128, 1, 0, 0, 0, 4, 0, 1}, {3, 128, 1, 1, 0, 0, 4, 0, 1},
-      {3, 128, 0, 0, 0, 0, 4, 0}, {3, 128, 0, 0, 0, 1, 4, 0}, {2, 256, 0, 0, 0, 1, 4, 0}, {4, 64, 0, 0, 0, 1, 4, 0},
-      {3, 128, 0, 0, 0, 1, 1, 0}, {3, 128, 0, 0, 0, 1, 8, 0},
-      {3, 128, 0, 0, 0, 2, 4, 0}, {3, 128, 0, 0, 0, 2, 4, 1}, {3, 128, 0, 0, 0, 2, 4, 2}, {3, 128, 0, 0, 0, 2, 4, 3},
-      {3, 128, 0, 0, 1, 2, 4, 2}, {3, 128, 0, 0, 1, 0, 4, 2}, {3, 128, 0, 0, 0, 0, 4, 1},
-      {2, 128, 0, 0, 0, 2, 4, 0}, {4, 128, 0, 0, 0, 2, 4, 0}, {4, 128, 0, 0, 0, 2, 4, 1},
+      {3, 128, 2, 0, 0, 0, 4, 0, 1, 3}, {6, 64, 2, 0, 0, 0, 4, 0, 1, 3}, {4, 64, 2, 0, 0, 0, 4, 0, 1, 2},
+      {3, 128, 1, 0, 0, 0, 4, 0, 1, 3}, {6, 64, 1, 0, 0, 0, 4, 0, 1, 3},
+      {3, 128, 0, 0, 0, 0, 4, 0, 1, 3}, {6, 64, 0, 0, 0, 0, 4, 0, 1, 3},
+      {3, 128, 2, 0, 0, 0, 4, 0, 0, 3}, {6, 64, 2, 0, 0, 0, 4, 0, 0, 3},
   };
   for (const V& v : vs) {
-    Opt o{v.nbuf, v.ncols, v.work, v.early, v.spin, 3 * 4 * 64, v.mode, v.kst, v.cmode, v.lean};
-    const int nthreads = 128 * v.nbuf + 32;
+    Opt o{v.nbuf, v.ncols, v.work, v.early, v.spin, 3 * 4 * 64 * (128 / v.ncols), v.mode, v.kst, v.cmode, v.lean, v.nwg};
+    const int nthreads = 128 * (v.nwg ? v.nwg : v.nbuf) + 32;
     pipe_kernel<<<148, nthreads, 80 * 1024>>>(o, d_res, d_sink);
     cudaError_t e = cudaDeviceSynchronize();
     uint64_t h[148];
@@ -212,8 +212,8 @@ int main() {
       }
       printf("   issuer wait+issue %.0f | issue->wake %.0f | wake->free %.0f | issuer gap %.0f\n", a / n, b / n, c / n, d / n);
     }
-    printf("lean %d cmode %d mode %d ksteps %d nbuf %d N %3d work %d early %d spin %d: %s  %.0f cycles per tile, %.0f per 128 keys\n",
-           v.lean, v.cmode, v.mode, v.kst, v.nbuf, v.ncols, v.work, v.early, v.spin, cudaGetErrorString(e), (sum / 148) / o.ntiles, per128);
+    printf("nwg %d lean %d cmode %d mode %d ksteps %d nbuf %d N %3d work %d early %d spin %d: %s  %.0f cycles per tile, %.0f per 128 keys\n",
+           v.nwg, v.lean, v.cmode, v.mode, v.kst, v.nbuf, v.ncols, v.work, v.early, v.spin, cudaGetErrorString(e), (sum / 148) / o.ntiles, per128);
   }
   return 0;
 }
