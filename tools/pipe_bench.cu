@@ -28,15 +28,16 @@ struct Opt {
   int kst;       // MMA K steps per tile (4 = d 128)
   int cmode;     // consumer: 0 normal; 1 no TMEM loads; 2 spin waits; 3 no tcgen05 fences
   int lean;      // issuer: lane-0-only loop, counters instead of modulo, unrolled K steps
+  int kload;     // 1: a producer warp streams 16 KB K tiles (bulk copies from L2) through a 4-stage ring
   int nwg;       // consumer warpgroups (0: = nbuf); WG w takes tiles w, w + nwg, ... (buffer t % nbuf)
 };
 
 __device__ uint64_t g_tr[4][768];  // CTA 0 event clocks: issuer start, issuer issued, consumer woke, consumer freed
 
-__global__ void __launch_bounds__(544, 1) pipe_kernel(Opt o, uint64_t* res, int* sink) {
+__global__ void __launch_bounds__(544, 1) pipe_kernel(Opt o, uint64_t* res, int* sink, const uint8_t* kglob) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
-  __shared__ uint64_t bars[16];
+  __shared__ uint64_t bars[24];
   __shared__ uint32_t tslot;
   __shared__ uint8_t lut8[32];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -46,6 +47,7 @@ __global__ void __launch_bounds__(544, 1) pipe_kernel(Opt o, uint64_t* res, int*
   const int NWGC = o.nwg ? o.nwg : o.nbuf;
   if (threadIdx.x == 0) {
     for (int i = 0; i < 8; ++i) { mbar_init(s_full + i, 1); mbar_init(s_free + i, 4); }
+    for (int i = 16; i < 24; ++i) mbar_init(bars + i, 1);  // k_full[4], k_empty[4]
     fence_mbar_init();
   }
   if (threadIdx.x < 32) lut8[threadIdx.x] = (uint8_t)(255 >> (threadIdx.x / 4));
@@ -60,17 +62,40 @@ __global__ void __launch_bounds__(544, 1) pipe_kernel(Opt o, uint64_t* res, int*
   const int T = o.ntiles;
   const uint32_t bcols = (uint32_t)o.ncols;
   uint64_t t0 = clk();
-  if (warp == issuer_warp && o.lean) {
+  uint64_t* k_full = bars + 16;
+  uint64_t* k_empty = bars + 20;
+  if (warp == issuer_warp + 1) {
+    if (o.kload && lane == 0) {  // K producer: 16 KB per tile from an L2-resident buffer
+      uint32_t kph = 0;
+      for (int t = 0; t < T; ++t) {
+        const int st = t & 3;
+        if (t >= 4) { mbar_wait(k_empty + st, (kph >> st) & 1u); kph ^= 1u << st; }
+        mbar_expect_tx(k_full + st, 16384);
+        asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], 16384, [%2];"
+                     ::"r"(smem_u32(smem + 32768 + st * 16384)),
+                     "l"(kglob + ((size_t)(blockIdx.x * 7 + t) % 512) * 16384), "r"(smem_u32(k_full + st))
+                     : "memory");
+      }
+    }
+    __syncwarp();
+  } else if (warp == issuer_warp && o.lean) {
     if (lane == 0) {
       const uint32_t idq = idesc_i8(128, o.ncols > 256 ? 256 : o.ncols, true, true);
-      const uint64_t dq = sdesc(smem_u32(smem), 1024, 2), dk = sdesc(smem_u32(smem + 16384), 1024, 2);
-      uint32_t ph = 0;
+      const uint64_t dq = sdesc(smem_u32(smem), 1024, 2);
+      uint64_t dk = sdesc(smem_u32(smem + 16384), 1024, 2);
+      uint32_t ph = 0, kph = 0;
       int w = 0;
       uint32_t dt = tmem;
       for (int t = 0; t < T; ++t) {
         if (t >= NB && o.mode != 1) {
           mbar_wait(s_free + w, (ph >> w) & 1u);
           ph ^= 1u << w;
+        }
+        if (o.kload) {
+          const int st = t & 3;
+          mbar_wait(k_full + st, (kph >> st) & 1u);
+          kph ^= 1u << st;
+          dk = sdesc(smem_u32(smem + 32768 + st * 16384), 1024, 2);
         }
         tc_fence_after();
         if (o.mode == 2) {
@@ -80,6 +105,7 @@ __global__ void __launch_bounds__(544, 1) pipe_kernel(Opt o, uint64_t* res, int*
           mma_i8_ss(dt, dq + 2, dk + 2, idq, 1u);
           mma_i8_ss(dt, dq + 4, dk + 4, idq, 1u);
           mma_i8_ss(dt, dq + 6, dk + 6, idq, 1u);
+          if (o.kload) tc_commit(k_empty + (t & 3));
           if (o.mode == 0) tc_commit(s_full + w);
         }
         if (++w == NB) { w = 0; dt = tmem; } else dt += bcols;
@@ -181,18 +207,21 @@ int main() {
   int* d_sink;
   cudaMalloc(&d_res, 148 * 8);
   cudaMalloc(&d_sink, 4096 * 4);
-  cudaFuncSetAttribute(pipe_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 80 * 1024);
-  struct V { int nbuf, ncols, work, early, spin, mode, kst, cmode, lean, nwg; };
+  cudaFuncSetAttribute(pipe_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 112 * 1024);
+  uint8_t* kglob;
+  cudaMalloc(&kglob, 512 * 16384);
+  cudaMemset(kglob, 0x11, 512 * 16384);
+  struct V { int nbuf, ncols, work, early, spin, mode, kst, cmode, lean, kload, nwg; };
   const V vs[] = {
-      {3, 128, 2, 0, 0, 0, 4, 0, 1, 3}, {6, 64, 2, 0, 0, 0, 4, 0, 1, 3}, {4, 64, 2, 0, 0, 0, 4, 0, 1, 2},
-      {3, 128, 1, 0, 0, 0, 4, 0, 1, 3}, {6, 64, 1, 0, 0, 0, 4, 0, 1, 3},
-      {3, 128, 0, 0, 0, 0, 4, 0, 1, 3}, {6, 64, 0, 0, 0, 0, 4, 0, 1, 3},
-      {3, 128, 2, 0, 0, 0, 4, 0, 0, 3}, {6, 64, 2, 0, 0, 0, 4, 0, 0, 3},
+      {3, 128, 0, 0, 0, 0, 4, 0, 1, 0, 3}, {3, 128, 0, 0, 0, 0, 4, 0, 1, 1, 3},
+      {3, 128, 1, 0, 0, 0, 4, 0, 1, 0, 3}, {3, 128, 1, 0, 0, 0, 4, 0, 1, 1, 3},
+      {3, 128, 2, 0, 0, 0, 4, 0, 1, 0, 3}, {3, 128, 2, 0, 0, 0, 4, 0, 1, 1, 3},
+      {3, 128, 0, 0, 0, 1, 4, 0, 1, 0, 3}, {3, 128, 0, 0, 0, 1, 4, 0, 1, 1, 3},
   };
   for (const V& v : vs) {
-    Opt o{v.nbuf, v.ncols, v.work, v.early, v.spin, 3 * 4 * 64 * (128 / v.ncols), v.mode, v.kst, v.cmode, v.lean, v.nwg};
-    const int nthreads = 128 * (v.nwg ? v.nwg : v.nbuf) + 32;
-    pipe_kernel<<<148, nthreads, 80 * 1024>>>(o, d_res, d_sink);
+    Opt o{v.nbuf, v.ncols, v.work, v.early, v.spin, 3 * 4 * 64 * (128 / v.ncols), v.mode, v.kst, v.cmode, v.lean, v.kload, v.nwg};
+    const int nthreads = 128 * (v.nwg ? v.nwg : v.nbuf) + 64;
+    pipe_kernel<<<148, nthreads, 112 * 1024>>>(o, d_res, d_sink, kglob);
     cudaError_t e = cudaDeviceSynchronize();
     uint64_t h[148];
     cudaMemcpy(h, d_res, sizeof(h), cudaMemcpyDeviceToHost);
@@ -212,8 +241,8 @@ int main() {
       }
       printf("   issuer wait+issue %.0f | issue->wake %.0f | wake->free %.0f | issuer gap %.0f\n", a / n, b / n, c / n, d / n);
     }
-    printf("nwg %d lean %d cmode %d mode %d ksteps %d nbuf %d N %3d work %d early %d spin %d: %s  %.0f cycles per tile, %.0f per 128 keys\n",
-           v.nwg, v.lean, v.cmode, v.mode, v.kst, v.nbuf, v.ncols, v.work, v.early, v.spin, cudaGetErrorString(e), (sum / 148) / o.ntiles, per128);
+    printf("kload %d nwg %d lean %d cmode %d mode %d ksteps %d nbuf %d N %3d work %d early %d spin %d: %s  %.0f cycles per tile, %.0f per 128 keys\n",
+           v.kload, v.nwg, v.lean, v.cmode, v.mode, v.kst, v.nbuf, v.ncols, v.work, v.early, v.spin, cudaGetErrorString(e), (sum / 148) / o.ntiles, per128);
   }
   return 0;
 }
