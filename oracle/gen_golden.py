@@ -12,6 +12,8 @@ commits its outputs as small fixtures:
   tests/golden/stage_small.npz   full per-stage arrays for a few tiny cases
   tests/golden/configs.json      per-(b, head) scales, c_int and output
                                  digests for the five BASELINE configs
+  tests/golden/errors.json       the exception class (or "ok") the reference raises for
+                                 each call of tests/cases.py:error_cases()
   tests/golden/quant_only_cases.npz  quant_only_attention (pipeline.py:259-296)
                                  outputs and requantised P^ (float comparator)
   tests/golden/grouped_cases.npz index_softmax_grouped (softmax.py:309-399)
@@ -46,7 +48,7 @@ import numpy as np  # noqa: E402
 import intattn as ia  # noqa: E402  (the reference)
 from intattn import softmax as ref_sm  # noqa: E402
 
-from cases import case_inputs, case_list, digest  # noqa: E402
+from cases import case_inputs, case_list, digest, error_cases, run_error_case  # noqa: E402
 from paper_2511_21513_b200 import workloads  # noqa: E402
 
 
@@ -284,6 +286,13 @@ def quant_only_cases():
     np.savez_compressed(os.path.join(GOLD, "quant_only_cases.npz"), **out)
 
 
+def errors():
+    """Exception class per error case, straight from the reference."""
+    res = {name: run_error_case(fn, ia) for name, fn in error_cases().items()}
+    with open(os.path.join(GOLD, "errors.json"), "w") as f:
+        json.dump(res, f, indent=1, sort_keys=True)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--configs", default="C1,C2,C2h,C3,C4,C5")
@@ -294,6 +303,7 @@ def main():
     os.makedirs(GOLD, exist_ok=True)
     grouped_cases()
     quant_only_cases()
+    errors()
     if a.grouped_only:
         return
     with open(os.path.join(GOLD, "kats.json"), "w") as f:

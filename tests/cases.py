@@ -91,3 +91,79 @@ def case_inputs(case):
     if sp == "masked_rows" and L > 4:
         mask[::7, :] = True
     return q, k, v, mask
+
+
+def error_cases():
+    """Calls that the reference rejects (or accepts) -- the same lambda runs against the
+    reference package (oracle/gen_golden.py records the exception class it raises into
+    tests/golden/errors.json) and against this package (tests/test_gpu_errors.py).
+    ``m`` is the package module."""
+    f32 = np.float32
+    z = lambda *s: np.zeros(s, f32)  # noqa: E731
+    i8 = lambda *s: np.zeros(s, np.int8)  # noqa: E731
+    i32 = lambda *s: np.zeros(s, np.int32)  # noqa: E731
+
+    def lut(m):
+        return m.build_lut(5, 6.6)
+
+    return {
+        "quantize_nan": lambda m: m.quantize_symmetric(np.array([[np.nan, 1.0]], f32)),
+        "quantize_inf": lambda m: m.quantize_symmetric(np.array([[np.inf]], f32)),
+        "quantize_ok": lambda m: m.quantize_symmetric(np.array([[1.0, -2.0]], f32)),
+        "quantize_3d": lambda m: m.quantize_symmetric(z(2, 2, 2)),
+        "matmul_not_int8": lambda m: m.matmul_int8(z(2, 2), i8(2, 2)),
+        "matmul_k_mismatch": lambda m: m.matmul_int8(i8(2, 3), i8(2, 4)),
+        "matmul_ok": lambda m: m.matmul_int8(i8(2, 3), i8(4, 3)),
+        "gemm_qk_not_quantized": lambda m: m.gemm_qk(i8(2, 2), i8(2, 2)),
+        "gemm_qk_row_groups": lambda m: m.gemm_qk(
+            m.quantize_symmetric(np.ones((4, 2), f32)),
+            m.quantize_symmetric(np.ones((4, 2), f32), m.QuantGranularity.per_row_group(2))),
+        "gemm_pv_bad_p": lambda m: m.gemm_pv(i32(2, 2), i8(2, 3)),
+        "gemm_pv_mismatch": lambda m: m.gemm_pv(np.zeros((2, 2), np.uint8), i8(3, 3)),
+        "gemm_pv_not_square": lambda m: m.gemm_pv(np.zeros((2, 3), np.uint8), i8(3, 3)),
+        "build_lut_b1": lambda m: m.build_lut(1, 6.6),
+        "build_lut_b9": lambda m: m.build_lut(9, 6.6),
+        "build_lut_c0": lambda m: m.build_lut(5, 0.0),
+        "compute_c_int_bad_d": lambda m: m.compute_c_int(6.6, 0, 0.05, 0.04),
+        "compute_c_int_bad_scale": lambda m: m.compute_c_int(6.6, 64, 0.0, 0.04),
+        "softmax_not_square": lambda m: m.index_softmax(i32(2, 3), 10, lut(m)),
+        "softmax_not_int32": lambda m: m.index_softmax(z(2, 2), 10, lut(m)),
+        "softmax_c_zero": lambda m: m.index_softmax(i32(2, 2), 0, lut(m)),
+        "softmax_lut_type": lambda m: m.index_softmax(i32(2, 2), 10, [255, 0]),
+        "softmax_mask_shape": lambda m: m.index_softmax(i32(2, 2), 10, lut(m),
+                                                        mask=np.zeros((3, 3), bool)),
+        "softmax_ok": lambda m: m.index_softmax(np.array([[100, 40], [40, 100]], np.int32), 50,
+                                                lut(m)),
+        "grouped_groups_shape": lambda m: m.index_softmax_grouped(i32(3, 3), np.zeros(2, np.int64),
+                                                                  [0.01], 6.6, lut(m)),
+        "grouped_alpha_nonpositive": lambda m: m.index_softmax_grouped(
+            i32(3, 3), np.zeros(3, np.int64), [0.0], 6.6, lut(m)),
+        "grouped_group_out_of_range": lambda m: m.index_softmax_grouped(
+            i32(3, 3), np.array([0, 1, 2]), [0.01, 0.02], 6.6, lut(m)),
+        "grouped_no_alphas": lambda m: m.index_softmax_grouped(i32(3, 3), np.zeros(3, np.int64),
+                                                               [], 6.6, lut(m)),
+        "attention_shape_mismatch": lambda m: m.int_attention(z(4, 8), z(4, 8), z(5, 8)),
+        "attention_1d": lambda m: m.int_attention(z(4), z(4), z(4)),
+        "attention_mask_shape": lambda m: m.int_attention(z(4, 8), z(4, 8), z(4, 8),
+                                                          m.AttentionConfig(mask=np.zeros((3, 3), bool))),
+        "attention_col_groups": lambda m: m.int_attention(
+            z(4, 8), z(4, 8), z(4, 8),
+            m.AttentionConfig(granularity=m.QuantGranularity.per_col_group(4))),
+        "attention_nan": lambda m: m.int_attention(np.full((4, 8), np.nan, f32), z(4, 8), z(4, 8)),
+        "attention_ok": lambda m: m.int_attention(np.ones((4, 8), f32), np.ones((4, 8), f32),
+                                                  np.ones((4, 8), f32)),
+        "quant_only_shape_mismatch": lambda m: m.quant_only_attention(z(4, 8), z(4, 9), z(4, 8)),
+        "quant_only_ok": lambda m: m.quant_only_attention(np.ones((4, 8), f32), np.ones((4, 8), f32),
+                                                          np.ones((4, 8), f32)),
+        "granularity_bad_group": lambda m: m.QuantGranularity.per_row_group(0),
+        "dequantize_ok": lambda m: m.dequantize(m.quantize_symmetric(np.ones((2, 2), f32))),
+    }
+
+
+def run_error_case(fn, m):
+    """Class name of the exception the call raises, or 'ok'."""
+    try:
+        fn(m)
+    except Exception as e:  # noqa: BLE001
+        return type(e).__name__
+    return "ok"
