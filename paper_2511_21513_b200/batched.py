@@ -138,11 +138,12 @@ def _host_pipelined(q, k, v, *, causal, seq_lens, mask, cfg, out, check_finite, 
         oh = out
     else:
         oh = torch.empty((B, H, L, d), dtype=torch.float32, pin_memory=True)
-    # Q / O buffers double-buffered per chunk, K / V double-buffered per KV group (a
+    # Q / O buffers triple-buffered per chunk, K / V double-buffered per KV group (a
     # group's second half reads the K / V its first half brought in)
+    NS = 3  # Q / O slots: chunk i+3's copy only waits for chunk i's kernel
     slots = [{"q": torch.empty((1, per * G, L, d), dtype=torch.float32, device=dev),
               "o": torch.empty((1, per * G, L, d), dtype=torch.float32, device=dev)}
-             for _ in range(2)]
+             for _ in range(NS)]
     kvbuf = [{"k": torch.empty((1, per, L, d), dtype=torch.float32, device=dev),
               "v": torch.empty((1, per, L, d), dtype=torch.float32, device=dev)}
              for _ in range(2)]
@@ -151,9 +152,9 @@ def _host_pipelined(q, k, v, *, causal, seq_lens, mask, cfg, out, check_finite, 
     s_in, s_run, s_out = torch.cuda.Stream(), torch.cuda.Stream(), torch.cuda.Stream()
     for s in (s_in, s_run, s_out):
         s.wait_stream(main)
-    q_read = [None, None]   # last compute that read the slot's Q
+    q_read = [None] * NS    # last compute that read the slot's Q
     kv_read = [None, None]  # last compute that read the K / V buffer
-    drained = [None, None]  # device->host copy that last read the slot's output
+    drained = [None] * NS   # device->host copy that last read the slot's output
     errs = [] if check_finite else False
     # K / V buffer of every chunk (a new group starts at each chunk that sends K / V)
     kv_of, g = [], -1
@@ -164,7 +165,7 @@ def _host_pipelined(q, k, v, *, causal, seq_lens, mask, cfg, out, check_finite, 
 
     def h2d(i):
         b, j0, j1, qa, qb, send_kv = chunks[i]
-        si, kb = i % 2, kvbuf[kv_of[i]]
+        si, kb = i % NS, kvbuf[kv_of[i]]
         with torch.cuda.stream(s_in):
             if send_kv:
                 if kv_read[kv_of[i]] is not None:
@@ -183,7 +184,7 @@ def _host_pipelined(q, k, v, *, causal, seq_lens, mask, cfg, out, check_finite, 
     for i, (b, j0, j1, qa, qb, send_kv) in enumerate(chunks):
         if i + 1 < len(chunks):
             h2d(i + 1)
-        si = i % 2
+        si = i % NS
         nkv, nq = j1 - j0, qb - qa
         qs, os_ = slots[si]["q"][:, :nq], slots[si]["o"][:, :nq]
         kb = kvbuf[kv_of[i]]
