@@ -166,15 +166,27 @@ def _host_pipelined(q, k, v, *, causal, seq_lens, mask, cfg, out, check_finite, 
     def h2d(i):
         b, j0, j1, qa, qb, send_kv = chunks[i]
         si, kb = i % NS, kvbuf[kv_of[i]]
+        # rows at or beyond seq_lens[b] never influence a result (excluded from the
+        # amax, masked as keys, written as +0.0 as queries), so only valid rows cross
+        # PCIe: one contiguous block per head when the batch entry is padded
+        n = L if sl_h is None else int(sl_h[b])
+
+        def put(dst, src):
+            if n == L:
+                dst.copy_(src, non_blocking=True)
+            else:
+                for h in range(src.shape[1]):
+                    dst[0, h, :n].copy_(src[0, h, :n], non_blocking=True)
+
         with torch.cuda.stream(s_in):
             if send_kv:
                 if kv_read[kv_of[i]] is not None:
                     s_in.wait_event(kv_read[kv_of[i]])
-                kb["k"][:, :j1 - j0].copy_(kh[b:b + 1, j0:j1], non_blocking=True)
-                kb["v"][:, :j1 - j0].copy_(vh[b:b + 1, j0:j1], non_blocking=True)
+                put(kb["k"][:, :j1 - j0], kh[b:b + 1, j0:j1])
+                put(kb["v"][:, :j1 - j0], vh[b:b + 1, j0:j1])
             if q_read[si] is not None:
                 s_in.wait_event(q_read[si])
-            slots[si]["q"][:, :qb - qa].copy_(qh[b:b + 1, qa:qb], non_blocking=True)
+            put(slots[si]["q"][:, :qb - qa], qh[b:b + 1, qa:qb])
             loaded[i] = torch.cuda.Event()
             loaded[i].record(s_in)
 
