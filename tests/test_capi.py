@@ -125,3 +125,23 @@ def test_use32_holds_for_baseline_configs():
         for d in (64, 128):
             hp = _lib.softmax_params_host(ci, 2 * d * 127 * 127, 32)
             assert hp.use32 == 1 and hp.unc32 == 1
+
+
+# The reference package's public names (intattn/__init__.py:56-92, its __all__).
+REFERENCE_API = (
+    "AttentionConfig", "ClipThreshold", "ElementKindMismatchError", "ExpLut", "FidelityReport",
+    "LogitMatrix", "MalformedHeaderError", "MAX_HEAD_DIM", "MAX_SEQ_LEN", "PFormat",
+    "ProbMatrix", "QuantGranularity", "QuantizedMatrix", "StageTimings", "TensorIOError",
+    "TruncatedPayloadError", "build_lut", "compare", "compute_c_int", "dataflow_audit",
+    "dequantize", "gemm_pv", "gemm_qk", "gemm_real", "index_softmax",
+    "index_softmax_grouped", "int_attention", "load_tensor", "matmul_int8", "quant_only_attention",
+    "quantize_symmetric", "reference_attention", "reference_attention_timed", "round_half_away", "save_tensor",
+)
+
+
+def test_exports_every_reference_name():
+    """The drop-in exports each of the reference's 35 public names."""
+    import paper_2511_21513_b200 as ia
+    missing = [n for n in REFERENCE_API if not hasattr(ia, n)]
+    assert not missing, missing
+    assert len(REFERENCE_API) == 35
