@@ -95,15 +95,37 @@ def _pinned(x):
     return t
 
 
+def chunk_plan(B, H, Hkv, L, d):
+    """Chunks of the host pipeline: ~8+ chunks of whole KV groups (at least one KV head
+    each).  With one KV head per chunk and GQA, each group is sent as two sub-chunks
+    (K, V + the first half of its query heads, then the second half reusing the K / V
+    already on the device): halves the pipeline fill (first H2D) and drain (last
+    kernel + D2H) at no extra PCIe bytes.  Returns (KV heads per chunk, chunks) with
+    chunk = (b, kv j0, kv j1, q head lo, q head hi, sends K/V)."""
+    G = H // Hkv
+    unit_bytes = 4 * L * d * (G + 2)
+    per = max(1, min(Hkv, (B * Hkv * unit_bytes // 8) // unit_bytes))
+    chunks = []
+    for b in range(B):
+        for j in range(0, Hkv, per):
+            j1 = min(j + per, Hkv)
+            if j1 - j == 1 and G >= 2:
+                chunks.append((b, j, j1, j * G, j * G + G // 2, True))
+                chunks.append((b, j, j1, j * G + G // 2, j1 * G, False))
+            else:
+                chunks.append((b, j, j1, j * G, j1 * G, True))
+    return per, chunks
+
+
 def _host_pipelined(q, k, v, *, causal, seq_lens, mask, cfg, out, check_finite, numpy_in):
     """Host-resident inputs with per-head scales: stream the problem through the
     device in (batch, KV-head group) chunks -- split into two query-head halves
     sharing the group's K/V when a chunk is a single GQA group -- so the
     host->device copy of chunk i+1, the fused kernel on chunk i and the
-    device->host copy of chunk i-1 overlap (three CUDA streams, two device buffer
-    slots).  Per-head scales and
-    per-unit outputs depend only on the unit's own data, so every chunk's result
-    is bit-identical to the one-shot launch."""
+    device->host copy of chunk i-1 overlap (three CUDA streams; three Q / O slots,
+    two K / V buffers).  Per-head scales and per-unit outputs depend only on the
+    unit's own data, so every chunk's result is bit-identical to the one-shot
+    launch."""
     dev = E.require_device()
     qh, kh, vh = _pinned(q), _pinned(k), _pinned(v)
     B, H, L, d = qh.shape
@@ -119,21 +141,7 @@ def _host_pipelined(q, k, v, *, causal, seq_lens, mask, cfg, out, check_finite, 
         mt = to_device(mask).to(torch.bool)
         if tuple(mt.shape) != (L, L):
             raise ValueError(f"mask must be {L}x{L}, got {tuple(mt.shape)}")
-    # ~8+ chunks of whole KV groups (at least one KV head each).  With one KV head per
-    # chunk and GQA, each group is sent as two sub-chunks (K, V + the first half of its
-    # query heads, then the second half reusing the K/V already on the device): halves
-    # the pipeline fill (first H2D) and drain (last kernel + D2H) at no extra PCIe bytes.
-    unit_bytes = 4 * L * d * (G + 2)
-    per = max(1, min(Hkv, (B * Hkv * unit_bytes // 8) // unit_bytes))
-    chunks = []  # (b, kv j0, kv j1, q head lo, q head hi, sends K/V)
-    for b in range(B):
-        for j in range(0, Hkv, per):
-            j1 = min(j + per, Hkv)
-            if j1 - j == 1 and G >= 2:
-                chunks.append((b, j, j1, j * G, j * G + G // 2, True))
-                chunks.append((b, j, j1, j * G + G // 2, j1 * G, False))
-            else:
-                chunks.append((b, j, j1, j * G, j1 * G, True))
+    per, chunks = chunk_plan(B, H, Hkv, L, d)
     if out is not None and is_torch(out) and out.device.type == "cpu":
         oh = out
     else:

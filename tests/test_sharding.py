@@ -121,3 +121,31 @@ def test_single_process_no_dist():
     out, mine = sharding.sharded_attention(q, k, v, causal=True, compute=oracle_compute)
     want, _ = O.attention_batched(q, k, v, causal=True)
     assert np.array_equal(out.view(np.uint32), want.view(np.uint32))
+
+
+@pytest.mark.parametrize("B,H,Hkv,L,d", [(1, 32, 8, 16384, 128), (16, 16, 16, 7968, 64),
+                                         (64, 12, 12, 197, 64), (2, 4, 2, 300, 64),
+                                         (3, 6, 2, 100, 32), (1, 3, 3, 50, 8)])
+def test_host_chunk_plan_covers_every_unit_once(B, H, Hkv, L, d):
+    """Host pipeline chunk plan: every (b, query head) is computed exactly once, with
+    its own KV head's K / V sent by the chunk itself or by the previous chunk of the
+    same group, and K / V sent exactly once per (b, KV head)."""
+    from paper_2511_21513_b200.batched import chunk_plan
+    G = H // Hkv
+    per, chunks = chunk_plan(B, H, Hkv, L, d)
+    seen_q, seen_kv = set(), set()
+    last_kv = None
+    for (b, j0, j1, qa, qb, send_kv) in chunks:
+        assert j0 * G <= qa < qb <= j1 * G and j1 - j0 <= per
+        if send_kv:
+            for j in range(j0, j1):
+                assert (b, j) not in seen_kv
+                seen_kv.add((b, j))
+            last_kv = (b, j0, j1)
+        else:
+            assert last_kv == (b, j0, j1)  # reuses the previous chunk's K / V
+        for h in range(qa, qb):
+            assert (b, h) not in seen_q
+            seen_q.add((b, h))
+    assert seen_q == {(b, h) for b in range(B) for h in range(H)}
+    assert seen_kv == {(b, j) for b in range(B) for j in range(Hkv)}
