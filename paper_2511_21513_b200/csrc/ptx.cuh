@@ -55,7 +55,7 @@ __device__ __forceinline__ uint32_t mbar_try_wait(uint32_t bar, uint32_t parity)
 }
 
 // Wait for the phase with the given parity to complete.  A watchdog traps after
-// ~2^40 SM cycles (~9 min) so a protocol bug surfaces as a launch error instead of
+// ~2^36 SM cycles (~35 s) so a protocol bug surfaces as a launch error instead of
 // a hung GPU.  It is time-based: a suspended try_wait returns on any barrier event
 // of the CTA, so a spin count says nothing about elapsed time (a role that idles
 // through whole passes, or a kernel slowed down by a profiler's replay, would trip
@@ -66,7 +66,7 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   const long long t0 = clock64();
   uint32_t spins = 0;
   while (!mbar_try_wait(a, parity)) {
-    if ((++spins & 1023u) == 0 && clock64() - t0 > (1ll << 40)) __trap();
+    if ((++spins & 1023u) == 0 && clock64() - t0 > (1ll << 36)) __trap();
   }
 }
 
@@ -101,7 +101,7 @@ __device__ __forceinline__ void mbar_wait_spin(uint64_t* bar, uint32_t parity) {
   const long long t0 = clock64();
   uint32_t spins = 0;
   while (!mbar_poll(a, parity)) {
-    if ((++spins & 1023u) == 0 && clock64() - t0 > (1ll << 40)) __trap();
+    if ((++spins & 1023u) == 0 && clock64() - t0 > (1ll << 36)) __trap();
   }
 }
 
