@@ -226,3 +226,32 @@ def c_int_from_alpha(c: float, alpha: float) -> int:
     r = float(c) / float(alpha)
     ci = int(np.copysign(np.floor(abs(r) + 0.5), r))
     return max(1, min(ci, 1 << 52))
+
+
+def quant_only_attention(q, k, v, mask=None, p_scale=P_UINT8X255):
+    """The reference's quant-only comparator (pipeline.py:259-296, f32 numpy as the
+    reference computes it): int8 QK^T, real = f32(logits) * f32(alpha), stable f32
+    softmax (masked -> -inf, fully masked row -> 0; pipeline.py:119-127), requantise
+    floor(p * scale + 0.5) (pipeline.py:130-140), int8 P.V, out = f32(acc) * f32(s_v /
+    scale).  Returns (out, phat)."""
+    q = np.ascontiguousarray(q, np.float32)
+    k = np.ascontiguousarray(k, np.float32)
+    v = np.ascontiguousarray(v, np.float32)
+    d = q.shape[1]
+    qq, sq = quantize_tensor(q)
+    kq, sk = quantize_tensor(k)
+    vq, sv = quantize_tensor(v)
+    logits = qq.astype(np.int64) @ kq.astype(np.int64).T
+    alpha = np.float32(float(sq) * float(sk) / np.sqrt(d))
+    real = logits.astype(np.int32).astype(np.float32) * alpha
+    if mask is not None:
+        real = np.where(np.asarray(mask, bool), np.float32(-np.inf), real)
+    m = real.max(axis=1, keepdims=True)
+    m = np.where(np.isfinite(m), m, np.float32(0))
+    e = np.exp(real - m)
+    s = e.sum(axis=1, keepdims=True)
+    p = e / np.where(s == 0, np.float32(1), s)
+    phat = (p * np.float32(p_scale) + np.float32(0.5)).astype(np.uint8)
+    acc = phat.astype(np.int64) @ vq.astype(np.int64)
+    out = acc.astype(np.float32) * np.float32(float(sv) / p_scale)
+    return out, phat

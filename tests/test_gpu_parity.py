@@ -442,3 +442,30 @@ def test_single_row_and_single_key():
         out, _ = ia.int_attention(q, k, v)
         want = O.int_attention(q, k, v)
         assert np.array_equal(out.view(np.uint32), want.view(np.uint32))
+
+
+@pytest.mark.parametrize("i", range(24))
+def test_fuzz_quant_only_vs_oracle(i):
+    """Quant-only mode on seeded random single-head problems (shapes, masks, P formats,
+    magnitudes) against the f32 numpy restatement of the reference's comparator
+    (oracle.quant_only_attention, pinned bit-exact to the reference's fixtures), with
+    the tolerance of test_quant_only_fused_vs_reference."""
+    rng = np.random.default_rng(20_000 + i)
+    L = int(rng.integers(1, 600))
+    d = int(rng.choice([8, 32, 64, 100, 128, 256]))
+    mags = [np.float32(10.0 ** rng.uniform(-1.5, 1.5)) for _ in range(3)]
+    q, k, v = (rng.standard_normal((L, d), dtype=np.float32) * m for m in mags)
+    kind = int(rng.integers(0, 3))
+    mask = None if kind == 0 else (np.triu(np.ones((L, L), bool), 1) if kind == 1
+                                   else rng.random((L, L)) < 0.3)
+    pfv = 127 if rng.random() < 0.3 else 255
+    cfg = ia.AttentionConfig(p_format=ia.PFormat.INT8X127 if pfv == 127 else ia.PFormat.UINT8X255)
+    out, dbg = ia.quant_only_attention_batched(q[None, None], k[None, None], v[None, None],
+                                               mask=mask, cfg=cfg, debug=True)
+    want_out, want_p = O.quant_only_attention(q, k, v, mask, pfv)
+    ph = dbg["prob"][0].cpu().numpy().astype(np.int32)
+    diff = np.abs(ph - want_p.astype(np.int32))
+    assert diff.max() <= 1 and (diff > 0).mean() <= 0.01, (L, d, kind, pfv, diff.max(), (diff > 0).mean())
+    sv = float(O.quantize_tensor(v)[1])
+    bound = (diff > 0).sum(axis=1)[:, None] * 127.0 * sv / pfv + 1e-6
+    assert (np.abs(out[0, 0] - want_out) <= bound).all()

@@ -163,3 +163,19 @@ def test_oracle_grouped_softmax_matches_reference():
         got = O.index_softmax_grouped(G[key + "_logits"], G[key + "_groups"], cis, lut, mask,
                                       int(G[key + "_pf"]))
         assert np.array_equal(got, G[key + "_prob"]), key
+
+
+def test_oracle_quant_only_matches_reference():
+    """The numpy restatement of quant_only_attention reproduces the reference's own
+    outputs and requantised P^ (tests/golden/quant_only_cases.npz) exactly: same f32
+    numpy operations."""
+    import os
+    G = np.load(os.path.join(os.path.dirname(__file__), "golden", "quant_only_cases.npz"))
+    for i in range(int(G["n"])):
+        key = f"qo{i}"
+        mask = G[key + "_mask"]
+        mask = None if mask.size == 0 else mask
+        out, phat = O.quant_only_attention(G[key + "_q"], G[key + "_k"], G[key + "_v"], mask,
+                                           int(G[key + "_pf"]))
+        assert np.array_equal(phat, G[key + "_phat"]), key
+        assert np.array_equal(out.view(np.uint32), G[key + "_out"].view(np.uint32)), key
