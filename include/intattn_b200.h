@@ -85,7 +85,9 @@ int ia_quantize(const float* x, int64_t n_rowgroups, int64_t rows_per_group, int
  * the amax and written 0.  Slots (amax_bits / counters / scales, each
  * B*H + 2*B*Hkv long; amax_bits and counters caller-zeroed) are Q heads, then
  * K heads, then V heads.  Results are bit-identical to ia_quant_amax_rows +
- * ia_quant_scales + ia_quantize; each f32 element is read from HBM once. */
+ * ia_quant_scales + ia_quantize.  Large slabs: one launch, each f32 element read
+ * from HBM once (team barrier per slab, L2 re-read); many small slabs: an amax
+ * launch and a quantise launch. */
 int ia_quant_heads(const float* q, const float* k, const float* v, int64_t B, int64_t H,
                    int64_t Hkv, int64_t L, int64_t d, const int32_t* seq_lens, int8_t* qhat,
                    int8_t* khat, int8_t* vt, int64_t d_pad, int64_t l_pad, uint32_t* amax_bits,

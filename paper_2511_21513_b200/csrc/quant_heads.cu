@@ -12,6 +12,7 @@
 // [d_pad, l_pad] the fused kernel's P.V operand wants; padding rows / columns are 0.
 // Arithmetic is the same IEEE f32 sequence as quantize.cu (bit-identical results).
 #include <cstdint>
+#include <cstdlib>
 
 #include "common.cuh"
 
@@ -22,15 +23,23 @@ namespace {
 __device__ __forceinline__ float qh_scale(uint32_t amax_bits) {
   return __fdiv_rn(fmaxf(__uint_as_float(amax_bits), 1e-12f), 127.0f);  // quantize.py:113
 }
-__device__ __forceinline__ uint32_t qh_q(float x, float s) {
-  const float t = __fdiv_rn(x, s);               // quantize.py:121
+// q = clip(round_half_away(x / s), +-127) with the quotient numpy computes (IEEE f32
+// x / s, quantize.py:121).  t = x * (1/s) is within |t| 2^-23 <= 2^-16 of it (|t| <= 127
+// + an ulp); unless |t| is within 2^-15 of a rounding boundary k + 0.5 (where the exact
+// quotient is taken), both round to the same integer, and the f32 sum |t| + 0.5 stays
+// 2^-16 away from an integer, so the rounded result is the reference's bit for bit.
+__device__ __forceinline__ uint32_t qh_q(float x, float s, float rcp) {
+  float t = __fmul_rn(x, rcp);
+  const float at = fabsf(t);
+  if (fabsf(__fsub_rn(__fsub_rn(at, floorf(at)), 0.5f)) <= 3.0517578125e-05f) t = __fdiv_rn(x, s);
   float r = floorf(__fadd_rn(fabsf(t), 0.5f));   // rounding.py:21
   r = fminf(r, 127.0f);                          // quantize.py:122
   const int v = (int)r;
   return (uint32_t)(uint8_t)(int8_t)(t < 0.0f ? -v : v);
 }
-__device__ __forceinline__ uint32_t qh_pack4(float4 v, float s) {
-  return qh_q(v.x, s) | (qh_q(v.y, s) << 8) | (qh_q(v.z, s) << 16) | (qh_q(v.w, s) << 24);
+__device__ __forceinline__ uint32_t qh_pack4(float4 v, float s, float rcp) {
+  return qh_q(v.x, s, rcp) | (qh_q(v.y, s, rcp) << 8) | (qh_q(v.z, s, rcp) << 16) |
+         (qh_q(v.w, s, rcp) << 24);
 }
 __device__ __forceinline__ uint32_t qh_abs(float x) { return __float_as_uint(x) & 0x7fffffffu; }
 
@@ -48,6 +57,7 @@ struct QHArgs {
   int32_t* err;
   int64_t n_slabs;
   int n_teams, team;
+  int mode;  // 0: fused (team barrier), 1: amax only, 2: quantise only (slabs in reverse order)
 };
 
 constexpr int QH_THREADS = 512;
@@ -59,10 +69,14 @@ __global__ void __launch_bounds__(QH_THREADS, 3) quant_heads_kernel(const QHArgs
   extern __shared__ __align__(16) uint8_t tile[];  // [d_pad][QH_TILE_PITCH] (V^T blocks)
   const int T = a.team;
   const int team = blockIdx.x / T, rank = blockIdx.x - (blockIdx.x / T) * T;
+  // split modes: one slab per team, no barrier; the quantise pass walks the slabs in the
+  // reverse of the amax pass's order so its first reads hit the slabs still in L2
+  const int64_t s_first = a.mode == 2 ? a.n_slabs - 1 - team : team;
+  const int64_t s_step = a.mode == 0 ? a.n_teams : a.n_slabs;
   const int tid = threadIdx.x;
   const int64_t L = a.L, d = a.d;
   const int64_t d4 = d >> 2;
-  for (int64_t s = team; s < a.n_slabs; s += a.n_teams) {
+  for (int64_t s = s_first; s < a.n_slabs; s += s_step) {
     int ti = 0;
     int64_t g = s;
     while (ti < 2 && g >= a.ngroups[ti]) { g -= a.ngroups[ti]; ++ti; }
@@ -73,7 +87,7 @@ __global__ void __launch_bounds__(QH_THREADS, 3) quant_heads_kernel(const QHArgs
     }
     const float4* base = reinterpret_cast<const float4*>(a.x[ti] + g * L * d);
     // ---- pass A: max |x| over the valid rows (quantize.py:92-101)
-    const int64_t n4 = nvalid * d4;
+    const int64_t n4 = a.mode == 2 ? 0 : nvalid * d4;
     uint32_t m = 0;
     {
       // four independent 16-byte loads in flight per thread (HBM needs the MLP)
@@ -100,20 +114,28 @@ __global__ void __launch_bounds__(QH_THREADS, 3) quant_heads_kernel(const QHArgs
       m = warp_max_u32(m);
       if (tid == 0) {
         // NaN bit patterns sort above +inf: a non-finite element lifts m >= 0x7f800000
-        if (m >= 0x7f800000u) atomicOr(reinterpret_cast<unsigned int*>(a.err), 1u);
-        else if (m) atomicMax(a.amax + s, m);
-        __threadfence();
-        atomicAdd(a.count + s, 1);
-        // the team meets here: every CTA of the team is resident (grid <= occupancy)
-        while (*reinterpret_cast<volatile int32_t*>(a.count + s) < T) __nanosleep(128);
-        __threadfence();
-        const float sc = qh_scale(*reinterpret_cast<volatile uint32_t*>(a.amax + s));
-        s_sh = sc;
-        if (rank == 0) a.scales[s] = sc;
+        if (a.mode != 2) {
+          if (m >= 0x7f800000u) atomicOr(reinterpret_cast<unsigned int*>(a.err), 1u);
+          else if (m) atomicMax(a.amax + s, m);
+        }
+        if (a.mode == 0) {
+          __threadfence();
+          atomicAdd(a.count + s, 1);
+          // the team meets here: every CTA of the team is resident (grid <= occupancy)
+          while (*reinterpret_cast<volatile int32_t*>(a.count + s) < T) __nanosleep(128);
+          __threadfence();
+        }
+        if (a.mode != 1) {
+          const float sc = qh_scale(*reinterpret_cast<volatile uint32_t*>(a.amax + s));
+          s_sh = sc;
+          if (rank == 0) a.scales[s] = sc;
+        }
       }
     }
     __syncthreads();
+    if (a.mode == 1) continue;  // amax only
     const float sc = s_sh;
+    const float rc = __frcp_rn(sc);
     // ---- pass B: quantise (slab re-read from L2)
     if (!a.transpose[ti]) {
       const int cpr = (int)(a.d_pad >> 4);  // 16-byte output chunks per row
@@ -127,10 +149,10 @@ __global__ void __launch_bounds__(QH_THREADS, 3) quant_heads_kernel(const QHArgs
           const float4* xr = base + r * d4 + (c0 >> 2);
           if (c0 + 16 <= d) {
             const float4 v0 = __ldg(xr), v1 = __ldg(xr + 1), v2 = __ldg(xr + 2), v3 = __ldg(xr + 3);
-            o = make_uint4(qh_pack4(v0, sc), qh_pack4(v1, sc), qh_pack4(v2, sc), qh_pack4(v3, sc));
+            o = make_uint4(qh_pack4(v0, sc, rc), qh_pack4(v1, sc, rc), qh_pack4(v2, sc, rc), qh_pack4(v3, sc, rc));
           } else {
             uint32_t w[4] = {0u, 0u, 0u, 0u};
-            for (int e = 0; e < 4 && c0 + 4 * e < d; ++e) w[e] = qh_pack4(__ldg(xr + e), sc);
+            for (int e = 0; e < 4 && c0 + 4 * e < d; ++e) w[e] = qh_pack4(__ldg(xr + e), sc, rc);
             o = make_uint4(w[0], w[1], w[2], w[3]);
           }
         }
@@ -160,7 +182,7 @@ __global__ void __launch_bounds__(QH_THREADS, 3) quant_heads_kernel(const QHArgs
             const int t = t0 + u * QH_THREADS + tid;
             if (t < nld) {
               const int rr = t / (dp >> 2), c4 = (t - rr * (dp >> 2)) << 2;
-              const uint32_t q = ok[u] ? qh_pack4(x4[u], sc) : 0u;
+              const uint32_t q = ok[u] ? qh_pack4(x4[u], sc, rc) : 0u;
               tile[(c4 + 0) * QH_TILE_PITCH + rr] = (uint8_t)q;
               tile[(c4 + 1) * QH_TILE_PITCH + rr] = (uint8_t)(q >> 8);
               tile[(c4 + 2) * QH_TILE_PITCH + rr] = (uint8_t)(q >> 16);
@@ -234,6 +256,27 @@ extern "C" int ia_quant_heads(const float* q, const float* k, const float* v, in
   n_teams = n_teams > a.n_slabs ? a.n_slabs : n_teams;
   a.n_teams = (int)n_teams;
   a.team = (int)team;
+  a.mode = 0;
+  // Many small slabs (C3: 96 x 1 MB) spend more on team barriers than on bytes: run the
+  // amax and quantise passes as two barrier-free launches instead (IA_QH_SPLIT=0/1
+  // forces either form, for A/B checks).
+  static const int split_env = getenv("IA_QH_SPLIT") ? atoi(getenv("IA_QH_SPLIT")) : -1;
+  const bool split = split_env >= 0 ? split_env != 0 : (slab_bytes <= (1 << 20) && a.n_slabs >= 32);
+  if (split) {
+    // amax over every slab, then the quantise pass in reverse slab order; no barriers,
+    // so the grids need not be resident: ~128 KB of f32 per CTA
+    int64_t t2 = (slab_bytes + (128 << 10) - 1) >> 17;
+    t2 = t2 < 1 ? 1 : t2;
+    a.team = (int)t2;
+    a.n_teams = (int)a.n_slabs;
+    const uint64_t g2 = (uint64_t)a.n_slabs * t2;
+    a.mode = 1;
+    quant_heads_kernel<<<(unsigned)g2, QH_THREADS, smem, (cudaStream_t)stream>>>(a);
+    if (int r = check_launch("quant_heads_kernel (amax)")) return r;
+    a.mode = 2;
+    quant_heads_kernel<<<(unsigned)g2, QH_THREADS, smem, (cudaStream_t)stream>>>(a);
+    return check_launch("quant_heads_kernel (quantise)");
+  }
   quant_heads_kernel<<<(unsigned)(n_teams * team), QH_THREADS, smem, (cudaStream_t)stream>>>(a);
   return check_launch("quant_heads_kernel");
 }

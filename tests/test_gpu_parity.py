@@ -469,3 +469,33 @@ def test_fuzz_quant_only_vs_oracle(i):
     sv = float(O.quantize_tensor(v)[1])
     bound = (diff > 0).sum(axis=1)[:, None] * 127.0 * sv / pfv + 1e-6
     assert (np.abs(out[0, 0] - want_out) <= bound).all()
+
+
+def test_quant_heads_rounding_boundaries():
+    """Values placed on and one ulp either side of every x.5 quotient boundary (and the
+    127.5 clip) for several head scales: the one-launch quantiser's reciprocal fast path
+    must fall back to the IEEE quotient exactly where it matters."""
+    rng = np.random.default_rng(99)
+    H, L, d = 4, 512, 128
+    q = np.zeros((1, H, L, d), np.float32)
+    for h in range(H):
+        amax = np.float32(10.0 ** rng.uniform(-3, 3))
+        s = np.float32(max(amax, np.float32(1e-12)) / np.float32(127))
+        ks = np.arange(-127, 128, dtype=np.float32)
+        base = (ks + np.float32(0.5)) * s
+        vals = np.concatenate([base, np.nextafter(base, np.float32(np.inf)),
+                               np.nextafter(base, np.float32(-np.inf)), ks * s,
+                               rng.uniform(-1, 1, L * d).astype(np.float32) * amax])
+        vals = np.clip(vals, -amax, amax)[:L * d]
+        vals[0] = amax
+        q[0, h] = vals.reshape(L, d)
+    dev = torch.device("cuda", 0)
+    qt = torch.from_numpy(q).to(dev)
+    kt = qt[:, :2].contiguous()
+    a = E.prepare(qt, kt, kt, quant="fused")
+    b = E.prepare(qt, kt, kt, quant="split")
+    for x, y, nm in [(a.qhat, b.qhat, "qhat"), (a.khat, b.khat, "khat"), (a.vt, b.vt, "vt")]:
+        assert torch.equal(x, y), (nm, _first_diff(x.cpu().numpy(), y.cpu().numpy()))
+    for h in range(H):
+        qq, _ = O.quantize_tensor(q[0, h])
+        assert np.array_equal(a.qhat[h, :, :d].cpu().numpy(), qq), h
