@@ -132,6 +132,23 @@ __device__ __forceinline__ uint32_t q_pack4(float4 v, float s) {
          ((uint32_t)(uint8_t)q_value(v.z, s) << 16) | ((uint32_t)(uint8_t)q_value(v.w, s) << 24);
 }
 
+// q_value via x * (1/s), with the IEEE quotient only within 2^-15 of a k + 0.5 rounding
+// boundary (same result bit for bit; the argument is at quant_heads.cu:qh_q).
+__device__ __forceinline__ int8_t q_value_rcp(float x, float s, float rcp) {
+  float t = __fmul_rn(x, rcp);
+  const float at = fabsf(t);
+  if (fabsf(__fsub_rn(__fsub_rn(at, floorf(at)), 0.5f)) <= 3.0517578125e-05f) t = __fdiv_rn(x, s);
+  float r = floorf(__fadd_rn(fabsf(t), 0.5f));
+  r = fminf(r, 127.0f);
+  const int v = (int)r;
+  return (int8_t)(t < 0.0f ? -v : v);
+}
+__device__ __forceinline__ uint32_t q_pack4_rcp(float4 v, float s, float rcp) {
+  return (uint32_t)(uint8_t)q_value_rcp(v.x, s, rcp) | ((uint32_t)(uint8_t)q_value_rcp(v.y, s, rcp) << 8) |
+         ((uint32_t)(uint8_t)q_value_rcp(v.z, s, rcp) << 16) |
+         ((uint32_t)(uint8_t)q_value_rcp(v.w, s, rcp) << 24);
+}
+
 // Vectorised row-major fast path (ROWS mode, cols % 4 == 0, 16-byte aligned
 // input, out_pitch % 16 == 0): each thread produces one 16-byte output chunk
 // (4 float4 loads -> 16 int8), a row is out_pitch/16 consecutive threads.
@@ -152,13 +169,15 @@ __global__ void __launch_bounds__(256) quantize_rows_vec_kernel(
     uint4 o = make_uint4(0u, 0u, 0u, 0u);
     if (valid && c0 < cols) {
       const float s = scales[g / slot_div];
+      const float rc = __frcp_rn(s);
       const float4* xr = reinterpret_cast<const float4*>(x + r * cols + c0);
       if (c0 + 16 <= cols) {
         const float4 a = __ldg(xr), b = __ldg(xr + 1), c = __ldg(xr + 2), d = __ldg(xr + 3);
-        o = make_uint4(q_pack4(a, s), q_pack4(b, s), q_pack4(c, s), q_pack4(d, s));
+        o = make_uint4(q_pack4_rcp(a, s, rc), q_pack4_rcp(b, s, rc), q_pack4_rcp(c, s, rc),
+                       q_pack4_rcp(d, s, rc));
       } else {
         uint32_t w[4] = {0u, 0u, 0u, 0u};
-        for (int e = 0; e < 4 && c0 + 4 * e < cols; ++e) w[e] = q_pack4(__ldg(xr + e), s);
+        for (int e = 0; e < 4 && c0 + 4 * e < cols; ++e) w[e] = q_pack4_rcp(__ldg(xr + e), s, rc);
         o = make_uint4(w[0], w[1], w[2], w[3]);
       }
     }
@@ -182,6 +201,7 @@ __global__ void __launch_bounds__(256) quantize_rows_t_vec_kernel(
     nvalid = v < nvalid ? v : nvalid;
   }
   const float s = scales[g / slot_div];
+  const float rc = __frcp_rn(s);
   const float* xg = x + g * (int64_t)rows_per_group * cols;
 #pragma unroll
   for (int k = 0; k < 4; ++k) {  // 64 rows x 16 float4 = 1024 loads
@@ -189,7 +209,7 @@ __global__ void __launch_bounds__(256) quantize_rows_t_vec_kernel(
     const int rr = t >> 4, c4 = (t & 15) << 2;
     const int r = r0 + rr, c = c0 + c4;
     uint32_t q = 0;
-    if (r < nvalid && c < cols) q = q_pack4(__ldg(reinterpret_cast<const float4*>(xg + (int64_t)r * cols + c)), s);
+    if (r < nvalid && c < cols) q = q_pack4_rcp(__ldg(reinterpret_cast<const float4*>(xg + (int64_t)r * cols + c)), s, rc);
     tile[c4 + 0][rr] = (uint8_t)q;
     tile[c4 + 1][rr] = (uint8_t)(q >> 8);
     tile[c4 + 2][rr] = (uint8_t)(q >> 16);
