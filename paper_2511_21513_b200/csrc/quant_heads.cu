@@ -57,16 +57,16 @@ struct QHArgs {
   int32_t* err;
   int64_t n_slabs;
   int n_teams, team;
+  int kb;    // V^T block: keys per block (multiple of 16, kb/4 * d_pad/4 <= QH_THREADS)
   int mode;  // 0: fused (team barrier), 1: amax only, 2: quantise only (slabs in reverse order)
 };
 
 constexpr int QH_THREADS = 512;
-constexpr int QH_TILE_PITCH = 64 + 16;  // transpose tile row pitch (bytes)
 
 __global__ void __launch_bounds__(QH_THREADS, 3) quant_heads_kernel(const QHArgs a) {
   __shared__ uint32_t red[QH_THREADS / 32];
   __shared__ float s_sh;
-  extern __shared__ __align__(16) uint8_t tile[];  // [d_pad][QH_TILE_PITCH] (V^T blocks)
+  extern __shared__ __align__(16) uint8_t tile[];  // [d_pad][kb + 4] bytes (V^T blocks)
   const int T = a.team;
   const int team = blockIdx.x / T, rank = blockIdx.x - (blockIdx.x / T) * T;
   // split modes: one slab per team, no barrier; the quantise pass walks the slabs in the
@@ -159,44 +159,44 @@ __global__ void __launch_bounds__(QH_THREADS, 3) quant_heads_kernel(const QHArgs
         *reinterpret_cast<uint4*>(og + r * a.d_pad + c0) = o;
       }
     } else {
-      // V^T: 64-key blocks, quantised along d, transposed through smem, stored as
-      // 16-byte runs of keys for each of the d_pad output rows
+      // V^T: blocks of kb keys.  Each thread loads a 4-key x 4-column patch (four
+      // float4, one per key), quantises it, transposes it in registers into four words
+      // (four keys of one column) and writes them to the tile [d_pad][kb/4 + 1 words];
+      // the odd pitch spreads the scatter over the banks.  The tile then leaves as
+      // 16-byte runs of keys for each of the d_pad output rows.
       int8_t* og = a.out[ti] + g * a.d_pad * a.l_pad;
-      const int nblk = (int)((a.l_pad + 63) >> 6);
-      const int dp = (int)a.d_pad;
+      uint32_t* tw = reinterpret_cast<uint32_t*>(tile);
+      const int dp = (int)a.d_pad, cg = dp >> 2, kb = a.kb, pw = (kb >> 2) + 1;
+      const int items = (kb >> 2) * cg;  // patches per block (<= QH_THREADS)
+      const int nblk = (int)((a.l_pad + kb - 1) / kb);
       for (int rb = rank; rb < nblk; rb += T) {
-        const int64_t r0 = (int64_t)rb * 64;
-        const int nld = 64 * (dp >> 2);  // float4 loads per block (<= 4096)
-        for (int t0 = 0; t0 < nld; t0 += 4 * QH_THREADS) {
+        const int64_t r0 = (int64_t)rb * kb;
+        if (tid < items) {
+          const int rg = tid / cg, c4 = (tid - rg * cg) << 2;
+          const int64_t rr = r0 + 4 * rg;
           float4 x4[4];
-          bool ok[4];
 #pragma unroll
-          for (int u = 0; u < 4; ++u) {  // all loads in flight before any use
-            const int t = t0 + u * QH_THREADS + tid;
-            const int rr = t / (dp >> 2), c4 = (t - rr * (dp >> 2)) << 2;
-            ok[u] = t < nld && r0 + rr < nvalid && c4 < d;
-            x4[u] = ok[u] ? __ldg(base + (r0 + rr) * d4 + (c4 >> 2)) : make_float4(0.f, 0.f, 0.f, 0.f);
-          }
+          for (int i = 0; i < 4; ++i)
+            x4[i] = (rr + i < nvalid && c4 < d) ? __ldg(base + (rr + i) * d4 + (c4 >> 2))
+                                                : make_float4(0.f, 0.f, 0.f, 0.f);
+          uint32_t w[4];
 #pragma unroll
-          for (int u = 0; u < 4; ++u) {
-            const int t = t0 + u * QH_THREADS + tid;
-            if (t < nld) {
-              const int rr = t / (dp >> 2), c4 = (t - rr * (dp >> 2)) << 2;
-              const uint32_t q = ok[u] ? qh_pack4(x4[u], sc, rc) : 0u;
-              tile[(c4 + 0) * QH_TILE_PITCH + rr] = (uint8_t)q;
-              tile[(c4 + 1) * QH_TILE_PITCH + rr] = (uint8_t)(q >> 8);
-              tile[(c4 + 2) * QH_TILE_PITCH + rr] = (uint8_t)(q >> 16);
-              tile[(c4 + 3) * QH_TILE_PITCH + rr] = (uint8_t)(q >> 24);
-            }
-          }
+          for (int i = 0; i < 4; ++i) w[i] = (rr + i < nvalid && c4 < d) ? qh_pack4(x4[i], sc, rc) : 0u;
+          const uint32_t lo01 = __byte_perm(w[0], w[1], 0x5140), hi01 = __byte_perm(w[0], w[1], 0x7362);
+          const uint32_t lo23 = __byte_perm(w[2], w[3], 0x5140), hi23 = __byte_perm(w[2], w[3], 0x7362);
+          tw[(c4 + 0) * pw + rg] = __byte_perm(lo01, lo23, 0x5410);
+          tw[(c4 + 1) * pw + rg] = __byte_perm(lo01, lo23, 0x7632);
+          tw[(c4 + 2) * pw + rg] = __byte_perm(hi01, hi23, 0x5410);
+          tw[(c4 + 3) * pw + rg] = __byte_perm(hi01, hi23, 0x7632);
         }
         __syncthreads();
-        for (int t = tid; t < dp * 4; t += QH_THREADS) {
-          const int c = t >> 2, u = (t & 3) << 4;
-          const int64_t r = r0 + u;
+        const int cpr = kb >> 4;  // 16-byte runs per output row
+        for (int t = tid; t < dp * cpr; t += QH_THREADS) {
+          const int c = t / cpr, u = t - c * cpr;
+          const int64_t r = r0 + 16 * u;
           if (r < a.l_pad) {
-            const uint32_t* tw = reinterpret_cast<const uint32_t*>(tile + c * QH_TILE_PITCH + u);
-            *reinterpret_cast<uint4*>(og + (int64_t)c * a.l_pad + r) = make_uint4(tw[0], tw[1], tw[2], tw[3]);
+            const uint32_t* src = tw + c * pw + 4 * u;
+            *reinterpret_cast<uint4*>(og + (int64_t)c * a.l_pad + r) = make_uint4(src[0], src[1], src[2], src[3]);
           }
         }
         __syncthreads();
@@ -237,21 +237,31 @@ extern "C" int ia_quant_heads(const float* q, const float* k, const float* v, in
   a.valid_rows = seq_lens;
   a.amax = amax_bits; a.count = counters; a.scales = scales; a.err = err_flag;
   a.n_slabs = B * H + 2 * B * Hkv;
-  const size_t smem = (size_t)d_pad * QH_TILE_PITCH;
+  // V^T block: one 4x4 patch per thread (kb * d_pad = 16 * QH_THREADS bytes)
+  static const int kb_env = getenv("IA_QH_KB") ? atoi(getenv("IA_QH_KB")) : 0;
+  int kb = (int)(((16 * QH_THREADS) / d_pad) & ~15);
+  if (kb_env >= 16 && (kb_env & 15) == 0 && (kb_env / 4) * (d_pad / 4) <= QH_THREADS) kb = kb_env;
+  a.kb = kb;
+  const size_t smem = (size_t)d_pad * (kb + 4);
+  void (*kern)(const QHArgs) = quant_heads_kernel;
   int per_sm = 0;
-  cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, quant_heads_kernel,
+  cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern,
                                                                 QH_THREADS, smem);
   if (e != cudaSuccess || per_sm < 1) return fail(IA_ERR_CUDA, "ia_quant_heads: occupancy query");
   // Team barriers need every CTA resident: the grid never exceeds one full wave.
   const int64_t grid_max = (int64_t)num_sms() * per_sm;
   const int64_t slab_bytes = L * d * 4;
   const int64_t slab_elems = L * d;
-  int64_t target = (64ll << 20) / (slab_bytes > 0 ? slab_bytes : 1);  // slabs in flight (~64 MB)
+  // IA_QH_L2MB / IA_QH_TEAM override the L2 budget and team size (A/B runs only)
+  static const int l2mb_env = getenv("IA_QH_L2MB") ? atoi(getenv("IA_QH_L2MB")) : 64;
+  static const int team_env = getenv("IA_QH_TEAM") ? atoi(getenv("IA_QH_TEAM")) : 0;
+  int64_t target = ((int64_t)l2mb_env << 20) / (slab_bytes > 0 ? slab_bytes : 1);  // slabs in flight (~64 MB)
   target = target < 1 ? 1 : (target > a.n_slabs ? a.n_slabs : target);
   int64_t team = grid_max / target;
   const int64_t want = (slab_elems + QH_THREADS * 16 - 1) / (QH_THREADS * 16);  // >= 16 elem/thread
   team = team < want ? team : want;
   team = team < 1 ? 1 : team;
+  if (team_env > 0) team = team_env < grid_max ? team_env : grid_max;
   int64_t n_teams = grid_max / team;
   n_teams = n_teams > a.n_slabs ? a.n_slabs : n_teams;
   a.n_teams = (int)n_teams;
@@ -271,12 +281,12 @@ extern "C" int ia_quant_heads(const float* q, const float* k, const float* v, in
     a.n_teams = (int)a.n_slabs;
     const uint64_t g2 = (uint64_t)a.n_slabs * t2;
     a.mode = 1;
-    quant_heads_kernel<<<(unsigned)g2, QH_THREADS, smem, (cudaStream_t)stream>>>(a);
+    kern<<<(unsigned)g2, QH_THREADS, smem, (cudaStream_t)stream>>>(a);
     if (int r = check_launch("quant_heads_kernel (amax)")) return r;
     a.mode = 2;
-    quant_heads_kernel<<<(unsigned)g2, QH_THREADS, smem, (cudaStream_t)stream>>>(a);
+    kern<<<(unsigned)g2, QH_THREADS, smem, (cudaStream_t)stream>>>(a);
     return check_launch("quant_heads_kernel (quantise)");
   }
-  quant_heads_kernel<<<(unsigned)(n_teams * team), QH_THREADS, smem, (cudaStream_t)stream>>>(a);
+  kern<<<(unsigned)(n_teams * team), QH_THREADS, smem, (cudaStream_t)stream>>>(a);
   return check_launch("quant_heads_kernel");
 }
