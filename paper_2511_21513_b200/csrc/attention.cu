@@ -53,7 +53,10 @@ struct AttnDev {
   long long* dbg_times;  // optional per-CTA phase clocks (development instrumentation)
   int B, H, Hkv, L, d, mask_words;
   int causal, nlut, scale_x2, n_qt;
-  int xflags;  // development experiments (IA_XFLAGS); 0 in production
+  // development experiments (IA_XFLAGS; 0 in production, results not exact otherwise):
+  // 1 pass 1 only; 2/4/8/16 spin instead of sleep-waits (QK^T issuer / softmax s_full /
+  // P.V issuer / TMA producers); 32 no pass-1 arithmetic; 256 generic index map (no magic9)
+  int xflags;
   uint8_t lut[256];
 };
 
