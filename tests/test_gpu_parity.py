@@ -212,11 +212,14 @@ def test_sharded_single_rank_gpu_tensor_scales():
     assert np.array_equal(out.view(np.uint32), want.view(np.uint32)), _first_diff(out, want)
 
 
-@pytest.mark.parametrize("B,H,Hkv,L,d,lens", [
-    (1, 1, 1, 128, 64, None), (2, 4, 2, 333, 128, [333, 100]), (1, 2, 1, 77, 20, None),
-    (3, 2, 2, 1000, 64, [1000, 0, 513]), (1, 8, 2, 4100, 128, None), (1, 1, 1, 64, 256, None),
-    (1, 2, 2, 200, 36, [150])])
-def test_quant_heads_matches_split(B, H, Hkv, L, d, lens):
+@pytest.mark.parametrize("B,H,Hkv,L,d,lens,d_pad", [
+    (1, 1, 1, 128, 64, None, None), (2, 4, 2, 333, 128, [333, 100], None), (1, 2, 1, 77, 20, None, None),
+    (3, 2, 2, 1000, 64, [1000, 0, 513], None), (1, 8, 2, 4100, 128, None, None),
+    (1, 1, 1, 64, 256, None, None), (1, 2, 2, 200, 36, [150], None),
+    # explicit d_pad: every V^T block width (kb = 16 * 512 / d_pad rounded to 16)
+    (1, 2, 1, 300, 40, None, 48), (2, 2, 2, 129, 16, [129, 7], 16), (1, 2, 2, 100, 80, None, 80),
+    (1, 1, 1, 257, 200, [250], 208), (1, 2, 1, 500, 128, [499], 144), (1, 1, 1, 33, 160, None, 176)])
+def test_quant_heads_matches_split(B, H, Hkv, L, d, lens, d_pad):
     """ia_quant_heads (one launch, team barriers) is bit-identical to the split
     amax + quantise kernels: Q^, K^, V^T (incl. padding) and every scale."""
     rng = np.random.default_rng(B * 1000 + L + d)
@@ -228,8 +231,8 @@ def test_quant_heads_matches_split(B, H, Hkv, L, d, lens):
     if lens is not None:
         lens = (lens * B)[:B]
         sl = torch.tensor(lens, dtype=torch.int32, device=dev)
-    a = E.prepare(q, k, v, seq_lens=sl, quant="fused")
-    b = E.prepare(q, k, v, seq_lens=sl, quant="split")
+    a = E.prepare(q, k, v, seq_lens=sl, quant="fused", d_pad=d_pad)
+    b = E.prepare(q, k, v, seq_lens=sl, quant="split", d_pad=d_pad)
     for x, y, nm in [(a.qhat, b.qhat, "qhat"), (a.khat, b.khat, "khat"), (a.vt, b.vt, "vt"),
                      (a.q_scales, b.q_scales, "sq"), (a.k_scales, b.k_scales, "sk"),
                      (a.v_scales, b.v_scales, "sv"),
