@@ -806,7 +806,15 @@ __global__ void __launch_bounds__(Cfg<DP>::NTHREADS, 1)
     const int rows = min(BM, p.L - q0);
     float* obase = p.out + ((size_t)bh * p.L + q0) * p.d;
     const int tid = threadIdx.x;
-    if ((p.d & 3) == 0) {
+    if (p.d == DP) {  // compile-time row pitch: shifts instead of a division
+      constexpr int D4 = DP / 4;
+#pragma unroll 1
+      for (int t = tid; t < rows * D4; t += NWT) {
+        const int r = t / D4, c4 = (t % D4) * 4;
+        const float* s4 = stage + r * C::STAGE_PITCH + c4;
+        *reinterpret_cast<float4*>(obase + (size_t)r * DP + c4) = make_float4(s4[0], s4[1], s4[2], s4[3]);
+      }
+    } else if ((p.d & 3) == 0) {
       const int d4 = p.d >> 2;
       for (int t = tid; t < rows * d4; t += NWT) {
         const int r = t / d4, c4 = (t - r * d4) << 2;
