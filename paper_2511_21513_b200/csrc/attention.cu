@@ -627,9 +627,20 @@ __global__ void __launch_bounds__(Cfg<DP>::NTHREADS, 1)
     for (int w = 1; w < NWG; ++w) S += xsum[w * 128 + row];
     // per-row normalisation table (softmax.py:157-160): (2*scale*lut[t] + S) // (2S)
     {
+      // num < 2^25 and 2S < 2^25 (S <= 255 * 65536): the f32 quotient is within 0.02
+      // of the exact one, so one remainder check makes it the exact floor
       const uint32_t two_s = 2u * S;
-      for (int t = wg; t < ntab; t += NWG) {  // t >= nlut: lut8[t] = 0 -> entry 0
-        const uint32_t pv = S ? ((uint32_t)p.scale_x2 * lut8[t] + S) / two_s : 0u;
+      const float rden = S ? __frcp_rn((float)two_s) : 0.0f;
+      for (int t = wg; t < ntab; t += NWG) {  // lut8[t] = 0 (incl. t >= nlut) -> S / 2S = 0
+        const uint32_t lt = lut8[t];
+        uint32_t pv = 0u;
+        if (S && lt) {
+          const uint32_t num = (uint32_t)p.scale_x2 * lt + S;
+          int32_t q = __float2int_rz(__fmul_rn((float)num, rden));
+          const int32_t r = (int32_t)num - q * (int32_t)two_s;
+          q += r < 0 ? -1 : (r >= (int32_t)two_s ? 1 : 0);
+          pv = (uint32_t)q;
+        }
         if (wtab) reinterpret_cast<uint32_t*>(tab)[t * 128 + row] = pv;
         else tab[t * 128 + row] = (uint8_t)pv;
       }
