@@ -9,6 +9,9 @@ v[b, h // g], AttentionConfig(mask=...))`` on the unit's valid rows
 """
 from __future__ import annotations
 
+import os
+from collections import OrderedDict
+
 import numpy as np
 import torch
 
@@ -95,6 +98,14 @@ def _pinned(x):
     return t
 
 
+# captured host-pipeline graphs (least recently used last); each holds its chunk buffers
+_GRAPHS: "OrderedDict[tuple, tuple]" = OrderedDict()
+_SEEN: set = set()
+_NO_GRAPH: set = set()
+_GRAPH_CACHE = 2
+_GRAPH_ON = os.environ.get("IA_NO_GRAPH", "0") != "1"
+
+
 def chunk_plan(B, H, Hkv, L, d):
     """Chunks of the host pipeline: ~8+ chunks of whole KV groups (at least one KV head
     each).  With one KV head per chunk and GQA, each group is sent as two sub-chunks
@@ -146,89 +157,133 @@ def _host_pipelined(q, k, v, *, causal, seq_lens, mask, cfg, out, check_finite, 
         oh = out
     else:
         oh = torch.empty((B, H, L, d), dtype=torch.float32, pin_memory=True)
-    # Q / O buffers triple-buffered per chunk, K / V double-buffered per KV group (a
-    # group's second half reads the K / V its first half brought in)
-    NS = 3  # Q / O slots: chunk i+3's copy only waits for chunk i's kernel
-    slots = [{"q": torch.empty((1, per * G, L, d), dtype=torch.float32, device=dev),
-              "o": torch.empty((1, per * G, L, d), dtype=torch.float32, device=dev)}
-             for _ in range(NS)]
-    kvbuf = [{"k": torch.empty((1, per, L, d), dtype=torch.float32, device=dev),
-              "v": torch.empty((1, per, L, d), dtype=torch.float32, device=dev)}
-             for _ in range(2)]
+    # lengths on the device before any capture (a pageable copy cannot be captured);
+    # a captured graph keeps them alive with its entry
     sl_d = None if sl_h is None else torch.as_tensor(sl_h.astype(np.int32)).to(dev)
-    main = torch.cuda.current_stream()
-    s_in, s_run, s_out = torch.cuda.Stream(), torch.cuda.Stream(), torch.cuda.Stream()
-    for s in (s_in, s_run, s_out):
-        s.wait_stream(main)
-    q_read = [None] * NS    # last compute that read the slot's Q
-    kv_read = [None, None]  # last compute that read the K / V buffer
-    drained = [None] * NS   # device->host copy that last read the slot's output
-    errs = [] if check_finite else False
-    # K / V buffer of every chunk (a new group starts at each chunk that sends K / V)
-    kv_of, g = [], -1
-    for c in chunks:
-        g += 1 if c[5] else 0
-        kv_of.append(g % 2)
-    loaded = [None] * len(chunks)
 
-    def h2d(i):
-        b, j0, j1, qa, qb, send_kv = chunks[i]
-        si, kb = i % NS, kvbuf[kv_of[i]]
-        # rows at or beyond seq_lens[b] never influence a result (excluded from the
-        # amax, masked as keys, written as +0.0 as queries), so only valid rows cross
-        # PCIe: one contiguous block per head when the batch entry is padded
-        n = L if sl_h is None else int(sl_h[b])
+    def enqueue():
+        """Every copy and launch of the call, stream-ordered (no host sync): run
+        eagerly, or captured once into a CUDA graph and replayed."""
+        # Q / O buffers triple-buffered per chunk, K / V double-buffered per KV group (a
+        # group's second half reads the K / V its first half brought in)
+        NS = 3  # Q / O slots: chunk i+3's copy only waits for chunk i's kernel
+        slots = [{"q": torch.empty((1, per * G, L, d), dtype=torch.float32, device=dev),
+                  "o": torch.empty((1, per * G, L, d), dtype=torch.float32, device=dev)}
+                 for _ in range(NS)]
+        kvbuf = [{"k": torch.empty((1, per, L, d), dtype=torch.float32, device=dev),
+                  "v": torch.empty((1, per, L, d), dtype=torch.float32, device=dev)}
+                 for _ in range(2)]
+        main = torch.cuda.current_stream()
+        s_in, s_run, s_out = torch.cuda.Stream(), torch.cuda.Stream(), torch.cuda.Stream()
+        for s in (s_in, s_run, s_out):
+            s.wait_stream(main)
+        q_read = [None] * NS    # last compute that read the slot's Q
+        kv_read = [None, None]  # last compute that read the K / V buffer
+        drained = [None] * NS   # device->host copy that last read the slot's output
+        errs = [] if check_finite else False
+        # K / V buffer of every chunk (a new group starts at each chunk that sends K / V)
+        kv_of, g = [], -1
+        for c in chunks:
+            g += 1 if c[5] else 0
+            kv_of.append(g % 2)
+        loaded = [None] * len(chunks)
 
-        def put(dst, src):
-            if n == L:
-                dst.copy_(src, non_blocking=True)
-            else:
-                for h in range(src.shape[1]):
-                    dst[0, h, :n].copy_(src[0, h, :n], non_blocking=True)
+        def h2d(i):
+            b, j0, j1, qa, qb, send_kv = chunks[i]
+            si, kb = i % NS, kvbuf[kv_of[i]]
+            # rows at or beyond seq_lens[b] never influence a result (excluded from the
+            # amax, masked as keys, written as +0.0 as queries), so only valid rows cross
+            # PCIe: one contiguous block per head when the batch entry is padded
+            n = L if sl_h is None else int(sl_h[b])
 
-        with torch.cuda.stream(s_in):
-            if send_kv:
-                if kv_read[kv_of[i]] is not None:
-                    s_in.wait_event(kv_read[kv_of[i]])
-                put(kb["k"][:, :j1 - j0], kh[b:b + 1, j0:j1])
-                put(kb["v"][:, :j1 - j0], vh[b:b + 1, j0:j1])
-            if q_read[si] is not None:
-                s_in.wait_event(q_read[si])
-            put(slots[si]["q"][:, :qb - qa], qh[b:b + 1, qa:qb])
-            loaded[i] = torch.cuda.Event()
-            loaded[i].record(s_in)
+            def put(dst, src):
+                if n == L:
+                    dst.copy_(src, non_blocking=True)
+                else:
+                    for h in range(src.shape[1]):
+                        dst[0, h, :n].copy_(src[0, h, :n], non_blocking=True)
 
-    # enqueue order H2D(i+1), kernel(i), D2H(i): the host never holds back the next
-    # chunk's copy behind this chunk's launch overhead
-    h2d(0)
-    for i, (b, j0, j1, qa, qb, send_kv) in enumerate(chunks):
-        if i + 1 < len(chunks):
-            h2d(i + 1)
-        si = i % NS
-        nkv, nq = j1 - j0, qb - qa
-        qs, os_ = slots[si]["q"][:, :nq], slots[si]["o"][:, :nq]
-        kb = kvbuf[kv_of[i]]
-        ks_, vs = kb["k"][:, :nkv], kb["v"][:, :nkv]
-        with torch.cuda.stream(s_run):
-            s_run.wait_event(loaded[i])
-            if drained[si] is not None:
-                s_run.wait_event(drained[si])
-            E.attention(qs, ks_, vs, causal=causal,
-                        seq_lens=None if sl_d is None else sl_d[b:b + 1], mask=mt,
-                        scale_granularity="head", b=cfg.b, c=cfg.c,
-                        p_scale=cfg.p_format.value, out=os_, check_finite=errs)
-            done = torch.cuda.Event()
-            done.record(s_run)
-            q_read[si] = done
-            kv_read[kv_of[i]] = done
-        with torch.cuda.stream(s_out):
-            s_out.wait_event(done)
-            oh[b:b + 1, qa:qb].copy_(os_, non_blocking=True)
-            ev = torch.cuda.Event()
-            ev.record(s_out)
-            drained[si] = ev
-    s_out.synchronize()
-    main.wait_stream(s_run)
-    if errs:  # one host sync for every chunk's non-finite flag
-        E.raise_if_nonfinite(torch.stack(errs).amax())
+            with torch.cuda.stream(s_in):
+                if send_kv:
+                    if kv_read[kv_of[i]] is not None:
+                        s_in.wait_event(kv_read[kv_of[i]])
+                    put(kb["k"][:, :j1 - j0], kh[b:b + 1, j0:j1])
+                    put(kb["v"][:, :j1 - j0], vh[b:b + 1, j0:j1])
+                if q_read[si] is not None:
+                    s_in.wait_event(q_read[si])
+                put(slots[si]["q"][:, :qb - qa], qh[b:b + 1, qa:qb])
+                loaded[i] = torch.cuda.Event()
+                loaded[i].record(s_in)
+
+        # enqueue order H2D(i+1), kernel(i), D2H(i): the host never holds back the next
+        # chunk's copy behind this chunk's launch overhead
+        h2d(0)
+        for i, (b, j0, j1, qa, qb, send_kv) in enumerate(chunks):
+            if i + 1 < len(chunks):
+                h2d(i + 1)
+            si = i % NS
+            nkv, nq = j1 - j0, qb - qa
+            qs, os_ = slots[si]["q"][:, :nq], slots[si]["o"][:, :nq]
+            kb = kvbuf[kv_of[i]]
+            ks_, vs = kb["k"][:, :nkv], kb["v"][:, :nkv]
+            with torch.cuda.stream(s_run):
+                s_run.wait_event(loaded[i])
+                if drained[si] is not None:
+                    s_run.wait_event(drained[si])
+                E.attention(qs, ks_, vs, causal=causal,
+                            seq_lens=None if sl_d is None else sl_d[b:b + 1], mask=mt,
+                            scale_granularity="head", b=cfg.b, c=cfg.c,
+                            p_scale=cfg.p_format.value, out=os_, check_finite=errs)
+                done = torch.cuda.Event()
+                done.record(s_run)
+                q_read[si] = done
+                kv_read[kv_of[i]] = done
+            with torch.cuda.stream(s_out):
+                s_out.wait_event(done)
+                oh[b:b + 1, qa:qb].copy_(os_, non_blocking=True)
+                ev = torch.cuda.Event()
+                ev.record(s_out)
+                drained[si] = ev
+        # join the side streams back into the calling (or capturing) stream
+        main.wait_stream(s_in)
+        main.wait_stream(s_run)
+        main.wait_stream(s_out)
+        return torch.stack(errs).amax() if errs else None
+
+    # Pinned host tensors (no mask): the whole call is one CUDA graph, captured on the
+    # second call with the same buffers and shapes and replayed after that, so the
+    # ~4 ms of per-chunk host work (Python, argument packing, tensor-map encoding)
+    # leaves the call and a busy host cannot starve the copy / compute pipeline.
+    key = None
+    if (mask is None and _GRAPH_ON and all(t.is_pinned() for t in (qh, kh, vh, oh))):
+        key = (dev.index, qh.data_ptr(), kh.data_ptr(), vh.data_ptr(), oh.data_ptr(),
+               tuple(qh.shape), tuple(kh.shape), None if sl_h is None else tuple(sl_h.tolist()),
+               bool(causal), cfg.b, cfg.c, cfg.p_format.value, bool(check_finite))
+    if key in _NO_GRAPH:
+        key = None
+    ent = _GRAPHS.get(key) if key is not None else None
+    if ent is None and key is not None and key in _SEEN:
+        g = torch.cuda.CUDAGraph()
+        try:
+            with torch.cuda.graph(g):
+                flag = enqueue()
+        except RuntimeError:  # capture refused: stay on the eager stream-ordered path
+            _NO_GRAPH.add(key)
+            key = None
+        else:
+            ent = _GRAPHS[key] = (g, flag, sl_d)
+            while len(_GRAPHS) > _GRAPH_CACHE:
+                _GRAPHS.popitem(last=False)
+    if ent is not None:
+        _GRAPHS.move_to_end(key)
+        g, flag, _ = ent
+        g.replay()
+        torch.cuda.current_stream().synchronize()
+    else:
+        if key is not None:
+            _SEEN.add(key)
+        flag = enqueue()
+        torch.cuda.current_stream().synchronize()
+    if flag is not None:  # one host read for every chunk's non-finite flag
+        E.raise_if_nonfinite(flag)
     return oh.numpy() if numpy_in else oh

@@ -502,3 +502,36 @@ def test_quant_heads_rounding_boundaries():
     for h in range(H):
         qq, _ = O.quantize_tensor(q[0, h])
         assert np.array_equal(a.qhat[h, :, :d].cpu().numpy(), qq), h
+
+
+def test_host_pipeline_graph_replay():
+    """Pinned host in / out: call 1 runs eagerly, call 2 captures the call into a CUDA
+    graph and replays it, later calls replay.  Every call is bit-exact with the device
+    path, including after the pinned inputs are overwritten in place (the graph reads
+    the buffers at replay time) and with a non-finite input (flag still raised)."""
+    from paper_2511_21513_b200 import batched
+    rng = np.random.default_rng(77)
+    B, H, Hkv, L, d = 2, 4, 2, 300, 64
+    lens = np.array([300, 171])
+    qh = torch.from_numpy(rng.standard_normal((B, H, L, d), dtype=np.float32)).pin_memory()
+    kh = torch.from_numpy(rng.standard_normal((B, Hkv, L, d), dtype=np.float32)).pin_memory()
+    vh = torch.from_numpy(rng.standard_normal((B, Hkv, L, d), dtype=np.float32)).pin_memory()
+    oh = torch.empty((B, H, L, d), dtype=torch.float32).pin_memory()
+
+    def want():
+        return ia.int_attention_batched(qh.cuda(), kh.cuda(), vh.cuda(), causal=True,
+                                        seq_lens=lens).cpu().numpy()
+
+    n0 = len(batched._GRAPHS)
+    for it in range(4):
+        if it == 3:  # new data in the same pinned buffers
+            qh.copy_(torch.from_numpy(rng.standard_normal((B, H, L, d), dtype=np.float32)))
+        got = ia.int_attention_batched(qh, kh, vh, causal=True, seq_lens=lens, out=oh)
+        assert got.data_ptr() == oh.data_ptr()
+        w = want()
+        assert np.array_equal(got.numpy().view(np.uint32), w.view(np.uint32)), it
+    assert len(batched._GRAPHS) == min(n0 + 1, batched._GRAPH_CACHE) or not batched._GRAPH_ON
+    kh[1, 0, 5, 3] = float("nan")
+    for _ in range(2):
+        with pytest.raises(ValueError):
+            ia.int_attention_batched(qh, kh, vh, causal=True, seq_lens=lens, out=oh)

@@ -1,40 +1,24 @@
-"""Host<->device copy rates and the pipelined host-in/host-out call (development tool)."""
-import os, sys, time
-sys.path.insert(0, os.path.join(os.path.dirname(__file__), ".."))
-import torch
-import paper_2511_21513_b200 as ia
-from paper_2511_21513_b200 import workloads
+"""Per-call wall time (ms) of the host-in/host-out API on one config, pinned buffers
+(IA_NO_GRAPH=1: the eager stream-ordered path instead of the captured graph)."""
+import os
+import sys
+import time
 
-wl = workloads.make("C4")
-qh = torch.from_numpy(wl.q).pin_memory(); kh = torch.from_numpy(wl.k).pin_memory()
-vh = torch.from_numpy(wl.v).pin_memory()
+sys.path.insert(0, os.path.join(os.path.dirname(os.path.abspath(__file__)), ".."))
+import torch  # noqa: E402
+
+import paper_2511_21513_b200 as ia  # noqa: E402
+from paper_2511_21513_b200 import workloads  # noqa: E402
+
+wl = workloads.make(sys.argv[1] if len(sys.argv) > 1 else "C4")
+qh, kh, vh = (torch.from_numpy(x).pin_memory() for x in (wl.q, wl.k, wl.v))
 oh = torch.empty(wl.q.shape, dtype=torch.float32).pin_memory()
-qd = torch.empty_like(qh, device="cuda")
-
-def t(fn, n=3):
-    fn(); torch.cuda.synchronize()
+for _ in range(3):
+    ia.int_attention_batched(qh, kh, vh, causal=wl.causal, seq_lens=wl.seq_lens, out=oh)
+rows = []
+for _ in range(int(sys.argv[2]) if len(sys.argv) > 2 else 30):
     t0 = time.perf_counter()
-    for _ in range(n):
-        fn()
-    torch.cuda.synchronize()
-    return (time.perf_counter() - t0) / n
-
-h2d = t(lambda: qd.copy_(qh, non_blocking=True))
-d2h = t(lambda: oh.copy_(qd, non_blocking=True))
-print(f"H2D {qh.numel()*4/h2d/1e9:.1f} GB/s  D2H {qh.numel()*4/d2h/1e9:.1f} GB/s")
-s2 = torch.cuda.Stream()
-def both():
-    qd.copy_(qh, non_blocking=True)
-    with torch.cuda.stream(s2):
-        oh.copy_(qd, non_blocking=True)
-    torch.cuda.current_stream().wait_stream(s2)
-bt = t(both)
-print(f"H2D+D2H concurrent 2x{qh.numel()*4/1e6:.0f} MB: {bt*1e3:.2f} ms")
-call = t(lambda: ia.int_attention_batched(qh, kh, vh, causal=True, out=oh))
-print(f"pipelined call {call*1e3:.2f} ms")
-from torch.profiler import profile, ProfilerActivity
-with profile(activities=[ProfilerActivity.CUDA, ProfilerActivity.CPU]) as prof:
-    ia.int_attention_batched(qh, kh, vh, causal=True, out=oh)
-    torch.cuda.synchronize()
-prof.export_chrome_trace("gpurun_out/e2e_trace.json")
-print(prof.key_averages().table(sort_by="cuda_time_total", row_limit=12))
+    ia.int_attention_batched(qh, kh, vh, causal=wl.causal, seq_lens=wl.seq_lens, out=oh)
+    t1 = time.perf_counter()
+    rows.append(1e3 * (t1 - t0))
+print(" ".join(f"{w:.2f}" for w in rows))
