@@ -100,7 +100,7 @@ def _pinned(x):
 
 # captured host-pipeline graphs (least recently used last); each holds its chunk buffers
 _GRAPHS: "OrderedDict[tuple, tuple]" = OrderedDict()
-_SEEN: set = set()
+_SEEN: "OrderedDict[tuple, None]" = OrderedDict()  # keys called once (eager), bounded
 _NO_GRAPH: set = set()
 _GRAPH_CACHE = 2
 _GRAPH_ON = os.environ.get("IA_NO_GRAPH", "0") != "1"
@@ -281,7 +281,9 @@ def _host_pipelined(q, k, v, *, causal, seq_lens, mask, cfg, out, check_finite, 
         torch.cuda.current_stream().synchronize()
     else:
         if key is not None:
-            _SEEN.add(key)
+            _SEEN[key] = None
+            while len(_SEEN) > 16:
+                _SEEN.popitem(last=False)
         flag = enqueue()
         torch.cuda.current_stream().synchronize()
     if flag is not None:  # one host read for every chunk's non-finite flag
