@@ -535,3 +535,19 @@ def test_host_pipeline_graph_replay():
     for _ in range(2):
         with pytest.raises(ValueError):
             ia.int_attention_batched(qh, kh, vh, causal=True, seq_lens=lens, out=oh)
+
+
+def test_host_pipeline_graph_refused_falls_back():
+    """Head dim > 256 takes the unfused path, whose host reads cannot be captured: the
+    capture is refused once and every call stays on the eager path, bit-exact."""
+    from paper_2511_21513_b200 import batched
+    rng = np.random.default_rng(78)
+    B, H, Hkv, L, d = 2, 2, 2, 40, 260
+    qh, kh, vh = (torch.from_numpy(rng.standard_normal((B, h, L, d), dtype=np.float32)).pin_memory()
+                  for h in (H, Hkv, Hkv))
+    oh = torch.empty((B, H, L, d), dtype=torch.float32).pin_memory()
+    w = ia.int_attention_batched(qh.cuda(), kh.cuda(), vh.cuda()).cpu().numpy()
+    for _ in range(3):
+        got = ia.int_attention_batched(qh, kh, vh, out=oh)
+        assert np.array_equal(got.numpy().view(np.uint32), w.view(np.uint32))
+    assert not any(k[1] == qh.data_ptr() for k in batched._GRAPHS)
