@@ -188,6 +188,13 @@ int ia_index_softmax_grouped(const int32_t* logits, int64_t rows, int64_t cols,
 int ia_gemm_i8(const void* A, int64_t lda, int a_signed, const int8_t* B, int64_t ldb,
                int64_t M, int64_t N, int64_t K, int32_t* C, int64_t ldc, void* stream);
 
+/* Host pipeline staging (no reference counterpart; the reference computes on the
+ * host): `height` rows of `width` bytes from src (pitch spitch) to dst (pitch dpitch),
+ * stream-ordered, either direction (cudaMemcpyDefault).  Used to move the valid rows
+ * of every head of a padded batch entry in one copy. */
+int ia_copy_rows_async(void* dst, int64_t dpitch, const void* src, int64_t spitch,
+                       int64_t width, int64_t height, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -33,7 +33,7 @@ EXPORTS = (
     "ia_quant_amax_rows", "ia_quant_amax_cols", "ia_quant_scales", "ia_quantize",
     "ia_dequantize", "ia_quant_heads", "ia_head_params_host", "ia_softmax_params_host", "ia_head_params_dev",
     "ia_mask_pack", "ia_attn_fwd", "ia_attn_supported", "ia_index_softmax", "ia_index_softmax_grouped",
-    "ia_gemm_i8",
+    "ia_gemm_i8", "ia_copy_rows_async",
 )
 
 
@@ -111,6 +111,7 @@ def load():
             "ia_index_softmax": ([P, i64, i64, ctypes.POINTER(HeadParams), P, i32, i32, P, P, P], i32),
             "ia_index_softmax_grouped": ([P, i64, i64, P, i32, P, P, i32, i32, P, P, P], i32),
             "ia_gemm_i8": ([P, i64, i32, P, i64, i64, i64, i64, P, i64, P], i32),
+            "ia_copy_rows_async": ([P, i64, P, i64, i64, i64, P], i32),
         }
         for name, (args, res) in sig.items():
             fn = getattr(L, name)

@@ -15,6 +15,7 @@ from collections import OrderedDict
 import numpy as np
 import torch
 
+from . import _lib
 from . import engine as E
 from ._tensors import is_torch, to_device, to_host
 from .gemm import MAX_SEQ_LEN
@@ -199,9 +200,11 @@ def _host_pipelined(q, k, v, *, causal, seq_lens, mask, cfg, out, check_finite, 
             def put(dst, src):
                 if n == L:
                     dst.copy_(src, non_blocking=True)
-                else:
-                    for h in range(src.shape[1]):
-                        dst[0, h, :n].copy_(src[0, h, :n], non_blocking=True)
+                elif n:  # the first n rows of every head: one pitched copy
+                    row = L * d * 4  # head stride of both [1, heads, L, d] views
+                    _lib.check(_lib.load().ia_copy_rows_async(
+                        dst.data_ptr(), row, src.data_ptr(), row, n * d * 4, src.shape[1],
+                        torch.cuda.current_stream().cuda_stream), "copy_rows")
 
             with torch.cuda.stream(s_in):
                 if send_kv:

@@ -148,3 +148,14 @@ extern "C" int ia_mask_pack(const uint8_t* mask, int64_t L, uint32_t* bits, void
   mask_pack_kernel<<<(unsigned)blocks, 256, 0, (cudaStream_t)stream>>>(mask, L, W, bits);
   return check_launch("mask_pack_kernel");
 }
+
+extern "C" int ia_copy_rows_async(void* dst, int64_t dpitch, const void* src, int64_t spitch,
+                                  int64_t width, int64_t height, void* stream) {
+  if (!dst || !src || width < 0 || height < 0 || dpitch < width || spitch < width)
+    return fail(IA_ERR_INVALID_ARGUMENT, "ia_copy_rows_async: bad arguments");
+  if (!width || !height) return IA_OK;
+  cudaError_t e = cudaMemcpy2DAsync(dst, (size_t)dpitch, src, (size_t)spitch, (size_t)width,
+                                    (size_t)height, cudaMemcpyDefault, (cudaStream_t)stream);
+  if (e != cudaSuccess) return fail(IA_ERR_CUDA, "ia_copy_rows_async: %s", cudaGetErrorString(e));
+  return IA_OK;
+}
