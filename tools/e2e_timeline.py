@@ -11,7 +11,7 @@ from torch.profiler import ProfilerActivity, profile  # noqa: E402
 import paper_2511_21513_b200 as ia  # noqa: E402
 from paper_2511_21513_b200 import workloads  # noqa: E402
 
-wl = workloads.make(sys.argv[1] if len(sys.argv) > 1 else "C5")
+wl = workloads.make(sys.argv[1] if len(sys.argv) > 1 and sys.argv[1] != "-v" else "C5")
 qh, kh, vh = (torch.from_numpy(x).pin_memory() for x in (wl.q, wl.k, wl.v))
 oh = torch.empty(wl.q.shape, dtype=torch.float32).pin_memory()
 for _ in range(3):
@@ -57,3 +57,6 @@ for k, v in spans.items():
     print(f"{k:7s} n={len(v):5d} busy {union(v) / 1e3:8.2f} ms  first {(min(a for a, _ in v) - t0) / 1e3:7.2f}  last end {(max(b for _, b in v) - t0) / 1e3:7.2f}")
 both = union(spans.get("h2d", [])) + union(spans.get("d2h", [])) - union(spans.get("h2d", []) + spans.get("d2h", []))
 print(f"h2d/d2h overlap {both / 1e3:.2f} ms")
+if "-v" in sys.argv:  # every copy / kernel interval, ms from the first
+    for e in sorted(ev, key=lambda e: e.time_range.start):
+        print(f"{kind(e):7s} {(e.time_range.start - t0) / 1e3:7.3f} {(e.time_range.end - t0) / 1e3:7.3f}  {e.name[:50]}")
