@@ -59,6 +59,7 @@ struct QHArgs {
   int n_teams, team;
   int kb;    // V^T block: keys per block (multiple of 16, kb/4 * d_pad/4 <= QH_THREADS)
   int mode;  // 0: fused (team barrier), 1: amax only, 2: quantise only (slabs in reverse order)
+  int pf;    // mode 0: bulk-prefetch the team's next slab into L2 before the team barrier
 };
 
 constexpr int QH_THREADS = 512;
@@ -104,6 +105,31 @@ __global__ void __launch_bounds__(QH_THREADS, 3) quant_heads_kernel(const QHArgs
       for (; i < n4; i += step) {
         const float4 v = __ldg(base + i);
         m = max(m, max(max(qh_abs(v.x), qh_abs(v.y)), max(qh_abs(v.z), qh_abs(v.w))));
+      }
+    }
+    if (a.pf && tid == 0 && s + s_step < a.n_slabs) {
+      // The next slab streams into L2 while this one waits at the barrier and runs
+      // pass B, so HBM stays busy across the team's serialising steps.  Each CTA of
+      // the team prefetches one contiguous 1/T of the next slab's valid rows.
+      const int64_t s2 = s + s_step;
+      int t2 = 0;
+      int64_t g2 = s2;
+      while (t2 < 2 && g2 >= a.ngroups[t2]) { g2 -= a.ngroups[t2]; ++t2; }
+      int64_t nv2 = L;
+      if (a.valid_rows) {
+        const int64_t v = a.valid_rows[g2 / a.valid_div[t2]];
+        nv2 = v < 0 ? 0 : (v < L ? v : L);
+      }
+      const int64_t bytes = nv2 * d * 4;
+      const int64_t per = ((bytes + T - 1) / T + 15) & ~(int64_t)15;
+      int64_t lo = (int64_t)rank * per, hi = lo + per;
+      hi = hi < bytes ? hi : bytes;
+      const char* p2 = reinterpret_cast<const char*>(a.x[t2] + g2 * L * d);
+      for (; lo < hi; lo += 32768) {
+        const int64_t n = (hi - lo < 32768 ? hi - lo : 32768) & ~(int64_t)15;
+        if (n > 0)
+          asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p2 + lo), "r"((uint32_t)n)
+                       : "memory");
       }
     }
     m = warp_max_u32(m);
@@ -267,6 +293,8 @@ extern "C" int ia_quant_heads(const float* q, const float* k, const float* v, in
   a.n_teams = (int)n_teams;
   a.team = (int)team;
   a.mode = 0;
+  static const int pf_env = getenv("IA_QH_PF") ? atoi(getenv("IA_QH_PF")) : 0;
+  a.pf = pf_env;
   // Many small slabs (C3: 96 x 1 MB) spend more on team barriers than on bytes: run the
   // amax and quantise passes as two barrier-free launches instead (IA_QH_SPLIT=0/1
   // forces either form, for A/B checks).
