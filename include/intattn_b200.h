@@ -92,6 +92,16 @@ int ia_quant_heads(const float* q, const float* k, const float* v, int64_t B, in
                    int64_t Hkv, int64_t L, int64_t d, const int32_t* seq_lens, int8_t* qhat,
                    int8_t* khat, int8_t* vt, int64_t d_pad, int64_t l_pad, uint32_t* amax_bits,
                    int32_t* counters, float* scales, int32_t* err_flag, void* stream);
+/* ia_quant_heads with per-TENSOR scales (QuantGranularity per-tensor,
+ * quantize.py:26-56,104-123: one max|x| over all heads of Q, of K, of V; the
+ * global-scale C2 config).  amax_bits (caller-zeroed) and scales hold 3 slots:
+ * Q, K, V.  Two launches (amax over every slab, then quantise from the three
+ * scales); bit-identical to ia_quant_amax_rows + ia_quant_scales + ia_quantize
+ * with one slot per tensor. */
+int ia_quant_tensors(const float* q, const float* k, const float* v, int64_t B, int64_t H,
+                     int64_t Hkv, int64_t L, int64_t d, const int32_t* seq_lens, int8_t* qhat,
+                     int8_t* khat, int8_t* vt, int64_t d_pad, int64_t l_pad, uint32_t* amax_bits,
+                     float* scales, int32_t* err_flag, void* stream);
 /* out = f32(values) * scale (quantize.py:126-128), same scale indexing. */
 int ia_dequantize(const int8_t* values, int64_t rows, int64_t cols, int mode,
                   int64_t group, const float* scales, float* out, void* stream);

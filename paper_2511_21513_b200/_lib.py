@@ -31,7 +31,7 @@ IA_QMODE_COLS = 1
 EXPORTS = (
     "ia_abi_version", "ia_status_string", "ia_last_error", "ia_device_check",
     "ia_quant_amax_rows", "ia_quant_amax_cols", "ia_quant_scales", "ia_quantize",
-    "ia_dequantize", "ia_quant_heads", "ia_head_params_host", "ia_softmax_params_host", "ia_head_params_dev",
+    "ia_dequantize", "ia_quant_heads", "ia_quant_tensors", "ia_head_params_host", "ia_softmax_params_host", "ia_head_params_dev",
     "ia_mask_pack", "ia_attn_fwd", "ia_attn_supported", "ia_index_softmax", "ia_index_softmax_grouped",
     "ia_gemm_i8", "ia_copy_rows_async",
 )
@@ -98,6 +98,8 @@ def load():
             "ia_quant_scales": ([P, i64, P, P], i32),
             "ia_quant_heads": ([P, P, P, i64, i64, i64, i64, i64, P, P, P, P, i64, i64, P, P, P,
                                 P, P], i32),
+            "ia_quant_tensors": ([P, P, P, i64, i64, i64, i64, i64, P, P, P, P, i64, i64, P, P,
+                                  P, P], i32),
             "ia_quantize": ([P, i64, i64, i64, P, i64, i32, i64, i64, P, P, i64, i32, i64, P], i32),
             "ia_dequantize": ([P, i64, i64, i32, i64, P, P, P], i32),
             "ia_head_params_host": ([ctypes.c_double, i64, i32, i32, ctypes.c_float,

@@ -59,6 +59,7 @@ struct QHArgs {
   int n_teams, team;
   int kb;    // V^T block: keys per block (multiple of 16, kb/4 * d_pad/4 <= QH_THREADS)
   int mode;  // 0: fused (team barrier), 1: amax only, 2: quantise only (slabs in reverse order)
+  int per_tensor;  // split modes only: one amax / scale slot per tensor (ti), not per slab
   int pf;    // mode 0: bulk-prefetch the team's next slab into L2 before the team barrier
 };
 
@@ -132,6 +133,7 @@ __global__ void __launch_bounds__(QH_THREADS, 3) quant_heads_kernel(const QHArgs
                        : "memory");
       }
     }
+    const int64_t slot = a.per_tensor ? ti : s;
     m = warp_max_u32(m);
     if ((tid & 31) == 0) red[tid >> 5] = m;
     __syncthreads();
@@ -142,7 +144,7 @@ __global__ void __launch_bounds__(QH_THREADS, 3) quant_heads_kernel(const QHArgs
         // NaN bit patterns sort above +inf: a non-finite element lifts m >= 0x7f800000
         if (a.mode != 2) {
           if (m >= 0x7f800000u) atomicOr(reinterpret_cast<unsigned int*>(a.err), 1u);
-          else if (m) atomicMax(a.amax + s, m);
+          else if (m) atomicMax(a.amax + slot, m);
         }
         if (a.mode == 0) {
           __threadfence();
@@ -152,9 +154,9 @@ __global__ void __launch_bounds__(QH_THREADS, 3) quant_heads_kernel(const QHArgs
           __threadfence();
         }
         if (a.mode != 1) {
-          const float sc = qh_scale(*reinterpret_cast<volatile uint32_t*>(a.amax + s));
+          const float sc = qh_scale(*reinterpret_cast<volatile uint32_t*>(a.amax + slot));
           s_sh = sc;
-          if (rank == 0) a.scales[s] = sc;
+          if (rank == 0) a.scales[slot] = sc;  // per tensor: every slab stores the same value
         }
       }
     }
@@ -237,12 +239,14 @@ __global__ void __launch_bounds__(QH_THREADS, 3) quant_heads_kernel(const QHArgs
 
 using namespace ia;
 
-extern "C" int ia_quant_heads(const float* q, const float* k, const float* v, int64_t B, int64_t H,
-                              int64_t Hkv, int64_t L, int64_t d, const int32_t* seq_lens,
-                              int8_t* qhat, int8_t* khat, int8_t* vt, int64_t d_pad, int64_t l_pad,
-                              uint32_t* amax_bits, int32_t* counters, float* scales,
-                              int32_t* err_flag, void* stream) {
-  if (!q || !k || !v || !qhat || !khat || !vt || !amax_bits || !counters || !scales || !err_flag)
+static int quant_heads_launch(const float* q, const float* k, const float* v, int64_t B,
+                              int64_t H, int64_t Hkv, int64_t L, int64_t d,
+                              const int32_t* seq_lens, int8_t* qhat, int8_t* khat, int8_t* vt,
+                              int64_t d_pad, int64_t l_pad, uint32_t* amax_bits,
+                              int32_t* counters, float* scales, int32_t* err_flag, void* stream,
+                              int per_tensor) {
+  if (!q || !k || !v || !qhat || !khat || !vt || !amax_bits || !scales || !err_flag ||
+      (!counters && !per_tensor))
     return fail(IA_ERR_INVALID_ARGUMENT, "ia_quant_heads: null pointer");
   if (B < 1 || H < 1 || Hkv < 1 || H % Hkv || L < 1 || d < 1)
     return fail(IA_ERR_INVALID_ARGUMENT, "ia_quant_heads: bad shape");
@@ -293,13 +297,16 @@ extern "C" int ia_quant_heads(const float* q, const float* k, const float* v, in
   a.n_teams = (int)n_teams;
   a.team = (int)team;
   a.mode = 0;
+  a.per_tensor = per_tensor;
   static const int pf_env = getenv("IA_QH_PF") ? atoi(getenv("IA_QH_PF")) : 0;
   a.pf = pf_env;
   // Many small slabs (C3: 96 x 1 MB) spend more on team barriers than on bytes: run the
   // amax and quantise passes as two barrier-free launches instead (IA_QH_SPLIT=0/1
   // forces either form, for A/B checks).
   static const int split_env = getenv("IA_QH_SPLIT") ? atoi(getenv("IA_QH_SPLIT")) : -1;
-  const bool split = split_env >= 0 ? split_env != 0 : (slab_bytes <= (1 << 20) && a.n_slabs >= 32);
+  // Per-tensor scales need every slab's amax first: always the two-launch form.
+  const bool split = per_tensor || (split_env >= 0 ? split_env != 0
+                                                   : (slab_bytes <= (1 << 20) && a.n_slabs >= 32));
   if (split) {
     // amax over every slab, then the quantise pass in reverse slab order; no barriers,
     // so the grids need not be resident: ~128 KB of f32 per CTA
@@ -317,4 +324,22 @@ extern "C" int ia_quant_heads(const float* q, const float* k, const float* v, in
   }
   kern<<<(unsigned)(n_teams * team), QH_THREADS, smem, (cudaStream_t)stream>>>(a);
   return check_launch("quant_heads_kernel");
+}
+
+extern "C" int ia_quant_heads(const float* q, const float* k, const float* v, int64_t B, int64_t H,
+                              int64_t Hkv, int64_t L, int64_t d, const int32_t* seq_lens,
+                              int8_t* qhat, int8_t* khat, int8_t* vt, int64_t d_pad, int64_t l_pad,
+                              uint32_t* amax_bits, int32_t* counters, float* scales,
+                              int32_t* err_flag, void* stream) {
+  return quant_heads_launch(q, k, v, B, H, Hkv, L, d, seq_lens, qhat, khat, vt, d_pad, l_pad,
+                            amax_bits, counters, scales, err_flag, stream, 0);
+}
+
+extern "C" int ia_quant_tensors(const float* q, const float* k, const float* v, int64_t B,
+                                int64_t H, int64_t Hkv, int64_t L, int64_t d,
+                                const int32_t* seq_lens, int8_t* qhat, int8_t* khat, int8_t* vt,
+                                int64_t d_pad, int64_t l_pad, uint32_t* amax_bits, float* scales,
+                                int32_t* err_flag, void* stream) {
+  return quant_heads_launch(q, k, v, B, H, Hkv, L, d, seq_lens, qhat, khat, vt, d_pad, l_pad,
+                            amax_bits, nullptr, scales, err_flag, stream, 1);
 }

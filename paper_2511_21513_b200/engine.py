@@ -180,6 +180,15 @@ def prepare(q, k, v, *, seq_lens=None, scale_granularity="head", b=5, c=6.6, p_s
             "quantize heads")
         return _finish_prepare(qhat, khat, vt, sq, sk, sv, ws, per_head, B, H, Hkv, d, b, c,
                                p_scale, d_pad, l_pad)
+    if quant == "fused" and scales is None and not per_head and d % 4 == 0 and d_pad <= 256 \
+            and d_pad % 16 == 0 and all(t.is_contiguous() and t.data_ptr() % 16 == 0
+                                        for t in (q, k, v)):
+        # per-tensor scales: one amax launch over Q, K, V + one quantise launch
+        _lib.check(_lib.load().ia_quant_tensors(
+            _p(q), _p(k), _p(v), B, H, Hkv, Lq, d, _p(sl), _p(qhat), _p(khat), _p(vt), d_pad,
+            l_pad, _p(ws.amax), _p(ws.scales), _p(ws.err), _stream()), "quantize tensors")
+        return _finish_prepare(qhat, khat, vt, sq, sk, sv, ws, per_head, B, H, Hkv, d, b, c,
+                               p_scale, d_pad, l_pad)
     if scales is None:
         amax_rows(q, B * H, Lq, d, aq, ws.err, seq_lens=sl, valid_div=H,
                   slot_div=1 if per_head else B * H)

@@ -241,6 +241,36 @@ def test_quant_heads_matches_split(B, H, Hkv, L, d, lens, d_pad):
     assert int(a.err.item()) == 0
 
 
+@pytest.mark.parametrize("B,H,Hkv,L,d,lens,zero_v", [
+    (64, 12, 12, 197, 64, None, False), (2, 4, 2, 333, 128, [333, 100], False),
+    (1, 2, 1, 77, 20, None, True), (3, 2, 2, 1000, 64, [1000, 0, 513], False),
+    (1, 8, 2, 4100, 128, None, False), (1, 2, 2, 200, 36, [150], False)])
+def test_quant_tensors_matches_split(B, H, Hkv, L, d, lens, zero_v):
+    """ia_quant_tensors (per-tensor scales: amax launch + quantise launch) is
+    bit-identical to the split amax + quantise kernels with one slot per tensor."""
+    rng = np.random.default_rng(7 * B + L + d)
+    dev = torch.device("cuda", 0)
+    q = torch.from_numpy(rng.standard_normal((B, H, L, d), dtype=np.float32) * 3).to(dev)
+    k = torch.from_numpy(rng.standard_normal((B, Hkv, L, d), dtype=np.float32)).to(dev)
+    v = torch.from_numpy(rng.standard_normal((B, Hkv, L, d), dtype=np.float32) * 0.1).to(dev)
+    q[..., ::17] *= 8.0  # outlier channels
+    if zero_v:
+        v.zero_()
+    sl = None
+    if lens is not None:
+        sl = torch.tensor((lens * B)[:B], dtype=torch.int32, device=dev)
+    a = E.prepare(q, k, v, seq_lens=sl, scale_granularity="tensor", quant="fused")
+    b = E.prepare(q, k, v, seq_lens=sl, scale_granularity="tensor", quant="split")
+    for x, y, nm in [(a.qhat, b.qhat, "qhat"), (a.khat, b.khat, "khat"), (a.vt, b.vt, "vt"),
+                     (a.q_scales, b.q_scales, "sq"), (a.k_scales, b.k_scales, "sk"),
+                     (a.v_scales, b.v_scales, "sv"),
+                     (a.params[:, :52], b.params[:, :52], "params")]:
+        assert torch.equal(x, y), (nm, _first_diff(x.cpu().numpy(), y.cpu().numpy()))
+    assert int(a.err.item()) == 0
+    k[0, -1, 3, 1] = float("inf")
+    assert int(E.prepare(q, k, v, scale_granularity="tensor").err.item()) == 1
+
+
 def test_quant_heads_nonfinite():
     dev = torch.device("cuda", 0)
     q = torch.randn(1, 2, 256, 64, device=dev)
