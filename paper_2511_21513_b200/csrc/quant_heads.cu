@@ -73,12 +73,13 @@ __global__ void __launch_bounds__(QH_THREADS, 3) quant_heads_kernel(const QHArgs
   const int team = blockIdx.x / T, rank = blockIdx.x - (blockIdx.x / T) * T;
   // split modes: one slab per team, no barrier; the quantise pass walks the slabs in the
   // reverse of the amax pass's order so its first reads hit the slabs still in L2
-  const int64_t s_first = a.mode == 2 ? a.n_slabs - 1 - team : team;
-  const int64_t s_step = a.mode == 0 ? a.n_teams : a.n_slabs;
+  // Teams stride over the slabs (split modes with n_teams == n_slabs: one slab each).
+  const int64_t s_step = a.n_teams;
   const int tid = threadIdx.x;
   const int64_t L = a.L, d = a.d;
   const int64_t d4 = d >> 2;
-  for (int64_t s = s_first; s < a.n_slabs; s += s_step) {
+  for (int64_t j = team; j < a.n_slabs; j += s_step) {
+    const int64_t s = a.mode == 2 ? a.n_slabs - 1 - j : j;
     int ti = 0;
     int64_t g = s;
     while (ti < 2 && g >= a.ngroups[ti]) { g -= a.ngroups[ti]; ++ti; }
@@ -108,7 +109,7 @@ __global__ void __launch_bounds__(QH_THREADS, 3) quant_heads_kernel(const QHArgs
         m = max(m, max(max(qh_abs(v.x), qh_abs(v.y)), max(qh_abs(v.z), qh_abs(v.w))));
       }
     }
-    if (a.pf && tid == 0 && s + s_step < a.n_slabs) {
+    if (a.pf && a.mode == 0 && tid == 0 && s + s_step < a.n_slabs) {
       // The next slab streams into L2 while this one waits at the barrier and runs
       // pass B, so HBM stays busy across the team's serialising steps.  Each CTA of
       // the team prefetches one contiguous 1/T of the next slab's valid rows.
@@ -314,7 +315,13 @@ static int quant_heads_launch(const float* q, const float* k, const float* v, in
     t2 = t2 < 1 ? 1 : t2;
     a.team = (int)t2;
     a.n_teams = (int)a.n_slabs;
-    const uint64_t g2 = (uint64_t)a.n_slabs * t2;
+    // IA_QH_WAVES=w > 0: at most w resident waves of teams, each striding over slabs
+    static const int waves_env = getenv("IA_QH_WAVES") ? atoi(getenv("IA_QH_WAVES")) : 0;
+    if (waves_env > 0) {
+      const int64_t cap = grid_max * waves_env / t2;
+      if (cap >= 1 && cap < a.n_slabs) a.n_teams = (int)cap;
+    }
+    const uint64_t g2 = (uint64_t)a.n_teams * t2;
     a.mode = 1;
     kern<<<(unsigned)g2, QH_THREADS, smem, (cudaStream_t)stream>>>(a);
     if (int r = check_launch("quant_heads_kernel (amax)")) return r;
