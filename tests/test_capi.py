@@ -53,6 +53,38 @@ def test_no_device_raises():
         ia.quantize_symmetric(x)
 
 
+def test_quant_entry_points_validate_before_device_work():
+    """ia_quant_heads / ia_quant_tensors reject null pointers, bad shapes and
+    misaligned operands with IA_ERR_INVALID_ARGUMENT before any CUDA call."""
+    L = _lib.load()
+    buf = (ctypes.c_uint8 * 4096)()
+    p = ctypes.addressof(buf)
+    p = (p + 15) & ~15
+    bad = _lib.IA_ERR_INVALID_ARGUMENT
+    # B, H, Hkv, L, d, d_pad, l_pad
+    good = (1, 2, 1, 16, 8, 16, 16)
+    cases = [((1, 2, 1, 16, 8, 16, 16), True),    # null operand
+             ((1, 3, 2, 16, 8, 16, 16), False),   # H % Hkv
+             ((1, 2, 1, 16, 6, 16, 16), False),   # d % 4
+             ((1, 2, 1, 16, 8, 8, 16), False),    # d_pad < d
+             ((1, 2, 1, 17, 8, 16, 16), False)]   # l_pad < L
+    for (B, H, Hkv, Lq, d, dp, lp), null in cases:
+        ptrs = [p] * 6
+        if null:
+            ptrs[1] = None
+        q, k, v, qh, kh, vt = ptrs
+        assert L.ia_quant_heads(q, k, v, B, H, Hkv, Lq, d, None, qh, kh, vt, dp, lp,
+                                p, p, p, p, None) == bad
+        assert L.ia_quant_tensors(q, k, v, B, H, Hkv, Lq, d, None, qh, kh, vt, dp, lp,
+                                  p, p, p, None) == bad
+    B, H, Hkv, Lq, d, dp, lp = good
+    assert L.ia_quant_tensors(p + 4, p, p, B, H, Hkv, Lq, d, None, p, p, p, dp, lp,
+                              p, p, p, None) == bad  # misaligned
+    assert L.ia_quant_heads(p, p, p, B, H, Hkv, Lq, d, None, p, p, p, dp, lp,
+                            p, None, p, p, None) == bad  # per-head needs counters
+    assert L.ia_last_error()
+
+
 @pytest.mark.parametrize("idx", range(0, len(stage_cases()), 7))
 def test_c_int_matches_reference(idx):
     row = stage_cases()[idx]
