@@ -16,6 +16,8 @@ commits its outputs as small fixtures:
                                  each call of tests/cases.py:error_cases()
   tests/golden/quant_only_cases.npz  quant_only_attention (pipeline.py:259-296)
                                  outputs and requantised P^ (float comparator)
+  tests/golden/audit.json        the dataflow_audit (tag, dtype) stream of the calls in
+                                 tests/cases.py:audit_cases()
   tests/golden/grouped_cases.npz index_softmax_grouped (softmax.py:309-399)
                                  inputs and outputs, incl. the grouped-K
                                  int_attention pipeline (pipeline.py:229-246)
@@ -48,7 +50,8 @@ import numpy as np  # noqa: E402
 import intattn as ia  # noqa: E402  (the reference)
 from intattn import softmax as ref_sm  # noqa: E402
 
-from cases import case_inputs, case_list, digest, error_cases, run_error_case  # noqa: E402
+from cases import (audit_cases, case_inputs, case_list, digest, error_cases,  # noqa: E402
+                   run_audit_case, run_error_case)
 from paper_2511_21513_b200 import workloads  # noqa: E402
 
 
@@ -293,14 +296,25 @@ def errors():
         json.dump(res, f, indent=1, sort_keys=True)
 
 
+def audits():
+    """dataflow_audit tag stream ((tag, dtype) per note) of each audited call."""
+    res = {name: run_audit_case(fn, ia) for name, fn in audit_cases().items()}
+    with open(os.path.join(GOLD, "audit.json"), "w") as f:
+        json.dump(res, f, indent=1, sort_keys=True)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--configs", default="C1,C2,C2h,C3,C4,C5")
     ap.add_argument("--skip-stages", action="store_true")
     ap.add_argument("--threads", type=int, default=os.cpu_count())
     ap.add_argument("--grouped-only", action="store_true")
+    ap.add_argument("--audit-only", action="store_true")
     a = ap.parse_args()
     os.makedirs(GOLD, exist_ok=True)
+    audits()
+    if a.audit_only:
+        return
     grouped_cases()
     quant_only_cases()
     errors()

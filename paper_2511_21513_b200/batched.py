@@ -68,15 +68,29 @@ def int_attention_batched(q, k, v, *, causal=False, seq_lens=None, mask=None,
         mt = to_device(mask).to(torch.bool)
         if tuple(mt.shape) != (L, L):
             raise ValueError(f"mask must be {L}x{L}, got {tuple(mt.shape)}")
-    o = None if out is None else out
+    host_out = out is not None and is_torch(out) and out.device.type == "cpu"
+    if out is not None and not is_torch(out):
+        raise TypeError("out must be a torch.Tensor")
+    if host_out and (out.dtype != torch.float32 or tuple(out.shape) != (B, H, L, d)
+                     or not out.is_contiguous()):
+        raise ValueError(f"out must be a contiguous float32 tensor of shape {(B, H, L, d)}")
+    # a CUDA ``out`` is validated (device, dtype, shape, contiguity) by E.attention
+    o = None if (out is None or host_out) else out
     res = E.attention(qt, kt, vt, causal=causal, seq_lens=sl, mask=mt,
                       scale_granularity=scale_granularity, b=cfg.b, c=cfg.c,
                       p_scale=cfg.p_format.value, out=o, debug=debug,
                       check_finite=check_finite, softmax=softmax)
+    dbg = None
     if debug:
         res, dbg = res
-        return to_host(res, numpy_in), dbg
-    return to_host(res, numpy_in)
+    if host_out:
+        out.copy_(res)
+        res = out
+        if numpy_in:
+            res = out.numpy()
+    else:
+        res = to_host(res, numpy_in)
+    return (res, dbg) if debug else res
 
 
 def quant_only_attention_batched(q, k, v, *, causal=False, seq_lens=None, mask=None,
@@ -154,7 +168,13 @@ def _host_pipelined(q, k, v, *, causal, seq_lens, mask, cfg, out, check_finite, 
         if tuple(mt.shape) != (L, L):
             raise ValueError(f"mask must be {L}x{L}, got {tuple(mt.shape)}")
     per, chunks = chunk_plan(B, H, Hkv, L, d)
-    if out is not None and is_torch(out) and out.device.type == "cpu":
+    if out is not None:
+        # host inputs -> host output: ``out`` must be a host f32 tensor of the result's
+        # shape (a CUDA ``out`` would silently not receive the result)
+        if not is_torch(out) or out.device.type != "cpu":
+            raise ValueError("with host inputs, out must be a CPU torch.Tensor")
+        if out.dtype != torch.float32 or tuple(out.shape) != (B, H, L, d) or not out.is_contiguous():
+            raise ValueError(f"out must be a contiguous float32 tensor of shape {(B, H, L, d)}")
         oh = out
     else:
         oh = torch.empty((B, H, L, d), dtype=torch.float32, pin_memory=True)

@@ -53,7 +53,8 @@ struct AttnDev {
   long long* dbg_times;  // optional per-CTA phase clocks (development instrumentation)
   int B, H, Hkv, L, d, mask_words;
   int causal, nlut, scale_x2, n_qt;
-  // development experiments (IA_XFLAGS; 0 in production, results not exact otherwise):
+  // development experiments (IA_XFLAGS, read only by the IA_PROFILE build; the release
+  // kernel compiles every XF() test to 0 -- results are not exact with any bit set):
   // 1 pass 1 only; 2/4/8/16 spin instead of sleep-waits (QK^T issuer / softmax s_full /
   // P.V issuer / TMA producers); 32 no pass-1 arithmetic; 256 generic index map (no magic9)
   int xflags;
@@ -135,9 +136,6 @@ __device__ __forceinline__ uint32_t lds_u32(uint32_t addr) {
 
 // Phase / wait-time instrumentation (tools/phase_times.py).  Compiled in only
 // for the profiling build (make profile -> libintattn_b200_prof.so).
-#ifndef IA_PROFILE
-#define IA_PROFILE 0
-#endif
 __device__ __forceinline__ long long clk64() {
 #if IA_PROFILE
   long long c;
@@ -147,6 +145,8 @@ __device__ __forceinline__ long long clk64() {
   return 0;
 #endif
 }
+// Experiment bits: compile-time 0 outside the profiling build.
+#define XF(bits) (IA_PROFILE ? (p.xflags & (bits)) : 0)
 #define IA_TMARK(slot)                                                                      \
   do {                                                                                      \
     if (IA_PROFILE && p.dbg_times) p.dbg_times[(size_t)blockIdx.x * 16 + (slot)] = clk64(); \
@@ -232,9 +232,9 @@ __global__ void __launch_bounds__(Cfg<DP>::NTHREADS, 1)
   const bool resident = n_kt <= NWG;  // every logit tile fits its own TMEM buffer
   // QO (quant-only comparator, pipeline.py:259-296): an online f32 max / sum-of-exp
   // pass, then the P / P.V pass -- two passes instead of IndexSoftmax's three.
-  const int npass = resident ? 1 : ((p.xflags & 1) ? 1 : (QO ? 2 : 3));
+  const int npass = resident ? 1 : ((XF(1)) ? 1 : (QO ? 2 : 3));
   constexpr int PV_PASS = QO ? 1 : 2;  // tile t >= PV_PASS * n_kt belongs to the P / P.V pass
-  const int n_kt_b = (p.xflags & 1) ? 0 : n_kt;  // key tiles of passes 2-3 / P.V
+  const int n_kt_b = (XF(1)) ? 0 : n_kt;  // key tiles of passes 2-3 / P.V
 
   if (rw == 0 && lane == 0) {
     prefetch_tmap(&tmq);
@@ -289,7 +289,7 @@ __global__ void __launch_bounds__(Cfg<DP>::NTHREADS, 1)
     const int t3 = PV_PASS * n_kt;
     const int nloads = npass * n_kt;
     for (int t = 0; t < nloads; ++t) {
-      bwait(k_empty + ks, ((kph >> ks) & 1u) ^ 1u, p.xflags & 16);
+      bwait(k_empty + ks, ((kph >> ks) & 1u) ^ 1u, XF(16));
       kph ^= 1u << ks;
       if (elect_one()) {
         IA_TRACE(0, 1, t);
@@ -308,7 +308,7 @@ __global__ void __launch_bounds__(Cfg<DP>::NTHREADS, 1)
     // ------------------------------------------------------------ V^T producer
     int vs = 0, vph = 0;
     for (int n = 0; n < n_kt_b; ++n) {
-      bwait(v_empty + vs, vph ^ 1, p.xflags & 16);
+      bwait(v_empty + vs, vph ^ 1, XF(16));
       if (elect_one()) {
         IA_TRACE(2, 5, n);
         mbar_expect_tx(v_full + vs, C::V_BYTES);
@@ -336,12 +336,12 @@ __global__ void __launch_bounds__(Cfg<DP>::NTHREADS, 1)
       const bool need_free = (used >> w) & 1u;
       const uint32_t f_ok = need_free ? mbar_test(s_free + w, (c_s >> w) & 1u) : 1u;
       const uint32_t k_ok = mbar_test(k_full + ks, (kph >> ks) & 1u);
-      if (!f_ok) bwait(s_free + w, (c_s >> w) & 1u, p.xflags & 2);
+      if (!f_ok) bwait(s_free + w, (c_s >> w) & 1u, XF(2));
       if (need_free) c_s ^= 1u << w;
       used |= 1u << w;
       if (lane == 0) IA_TRACE(1, 5, t);
       long long t1 = clk64();
-      if (!k_ok) bwait(k_full + ks, (kph >> ks) & 1u, p.xflags & 2);
+      if (!k_ok) bwait(k_full + ks, (kph >> ks) & 1u, XF(2));
       kph ^= 1u << ks;
       long long t2 = clk64();
       IA_TADD(8, t1 - t0);
@@ -376,9 +376,9 @@ __global__ void __launch_bounds__(Cfg<DP>::NTHREADS, 1)
     for (int n = 0; n < n_kt_b; ++n) {
       const int pb = w * C::NPB + tl % C::NPB;
       long long t0 = clk64();
-      bwait(p_full + pb, (uint32_t)(tl / C::NPB) & 1u, p.xflags & 8);
+      bwait(p_full + pb, (uint32_t)(tl / C::NPB) & 1u, XF(8));
       long long t1 = clk64();
-      bwait(v_full + vs, vph, p.xflags & 8);
+      bwait(v_full + vs, vph, XF(8));
       long long t2 = clk64();
       IA_TADD(11, t1 - t0);
       IA_TADD(12, t2 - t1);
@@ -431,7 +431,7 @@ __global__ void __launch_bounds__(Cfg<DP>::NTHREADS, 1)
     float qm = -INFINITY, qs = 0.0f;
     for (int n = wg; n < n_kt; n += NWG) {
       long long tw0 = clk64();
-      bwait(s_full + wg, s_ph, p.xflags & 4);
+      bwait(s_full + wg, s_ph, XF(4));
       if (trw) IA_TRACE(4 + warp, 8, 0 * n_kt + n);
       s_ph ^= 1u;
       if (tm) IA_TADD(15, clk64() - tw0);
@@ -484,7 +484,7 @@ __global__ void __launch_bounds__(Cfg<DP>::NTHREADS, 1)
             }
             qs += acc0 + acc1;
           }
-        } else if (p.xflags & 32) {  // experiment: no pass-1 arithmetic
+        } else if (XF(32)) {  // experiment: no pass-1 arithmetic
         } else if (!p.mask_bits) {
           if (!__any_sync(0xffffffffu, cut < 64)) {
 #pragma unroll
@@ -567,7 +567,7 @@ __global__ void __launch_bounds__(Cfg<DP>::NTHREADS, 1)
     for (int n = wg; n < (QO ? 0 : n_kt_b); n += NWG) {
       if (!resident) {
         long long tw0 = clk64();
-        bwait(s_full + wg, s_ph, p.xflags & 4);
+        bwait(s_full + wg, s_ph, XF(4));
         if (trw) IA_TRACE(4 + warp, 8, 1 * n_kt + n);
         s_ph ^= 1u;
         if (tm) IA_TADD(14, clk64() - tw0);
@@ -651,7 +651,7 @@ __global__ void __launch_bounds__(Cfg<DP>::NTHREADS, 1)
     const uint32_t tab_row = smem_u32(tab) + (uint32_t)row * (wtab ? 4u : 1u);
     const uint32_t tab_sh = wtab ? 9u : 7u;
     const uint32_t tab0 = smem_u32(tab), row4 = (uint32_t)row * 4u;
-    const uint32_t m9 = (wtab && !(p.xflags & 256)) ? hp.magic9 : 0u;
+    const uint32_t m9 = (wtab && !(XF(256))) ? hp.magic9 : 0u;
     // this thread's row of its warpgroup's P^ tile (K-major, 128B swizzle: 16-byte
     // unit x of row r lives at unit x ^ (r % 8))
     const uint32_t p_rows = smem_u32(smem + C::OFF_P + wg * C::NPB * C::P_BYTES) + (uint32_t)row * 128;
@@ -662,7 +662,7 @@ __global__ void __launch_bounds__(Cfg<DP>::NTHREADS, 1)
     for (int n = wg; n < n_kt_b; n += NWG) {
       if (!resident) {
         long long tw0 = clk64();
-        bwait(s_full + wg, s_ph, p.xflags & 4);
+        bwait(s_full + wg, s_ph, XF(4));
         if (trw) IA_TRACE(4 + warp, 8, 2 * n_kt + n);
         s_ph ^= 1u;
         if (tm) IA_TADD(14, clk64() - tw0);
@@ -900,7 +900,7 @@ static int launch_attn(const ia_attn_args* a, cudaStream_t st) {
   dv.nlut = a->nlut;
   dv.scale_x2 = 2 * a->p_scale;
   dv.n_qt = (int)((a->L + BM - 1) / BM);
-  static const int xflags = getenv("IA_XFLAGS") ? atoi(getenv("IA_XFLAGS")) : 0;
+  static const int xflags = dev_knob("IA_XFLAGS", 0);  // always 0 in the release build
   dv.xflags = xflags;
   for (int t = 0; t < 256; ++t) dv.lut[t] = t < a->nlut ? a->lut[t] : 0;
   size_t smem = attn_smem_bytes<DP>(a->nlut);
@@ -963,10 +963,11 @@ extern "C" int ia_attn_fwd(const ia_attn_args* a, void* stream) {
     case 32: return dbg ? launch_attn<32, true>(a, st) : launch_attn<32, false>(a, st);
     case 64: return dbg ? launch_attn<64, true>(a, st) : launch_attn<64, false>(a, st);
     case 128:
-      // IA_EXPERIMENT=skeleton: timing-only variant (softmax reads TMEM, skips the
-      // integer work; output is NOT IndexSoftmax).  Never used by the library API.
-      if (!dbg && getenv("IA_EXPERIMENT") && !strcmp(getenv("IA_EXPERIMENT"), "skeleton"))
-        return launch_attn<128, false, true>(a, st);
+#if IA_PROFILE
+      // IA_EXPERIMENT=1 (profiling build only): timing-only skeleton (softmax reads TMEM,
+      // skips the integer work; output is NOT IndexSoftmax).
+      if (!dbg && dev_knob("IA_EXPERIMENT", 0) == 1) return launch_attn<128, false, true>(a, st);
+#endif
       return dbg ? launch_attn<128, true>(a, st) : launch_attn<128, false>(a, st);
     default: return dbg ? launch_attn<256, true>(a, st) : launch_attn<256, false>(a, st);
   }

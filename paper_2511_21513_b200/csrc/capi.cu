@@ -5,6 +5,7 @@
 
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 
 #include "common.cuh"
@@ -26,6 +27,16 @@ int check_launch(const char* what) {
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return fail(IA_ERR_CUDA, "%s: %s", what, cudaGetErrorString(e));
   return IA_OK;
+}
+
+int dev_knob(const char* name, int dflt) {
+#if IA_PROFILE
+  const char* s = getenv(name);
+  return s ? atoi(s) : dflt;
+#else
+  (void)name;
+  return dflt;
+#endif
 }
 
 int num_sms() {

@@ -7,7 +7,16 @@
 
 #include "intattn_b200.h"
 
+#ifndef IA_PROFILE
+#define IA_PROFILE 0
+#endif
+
 namespace ia {
+
+// Development A/B switch: read from the environment ONLY in the profiling build
+// (make profile, -DIA_PROFILE=1); the release library always returns `dflt`, so no
+// environment variable can change what the production kernels compute or how.
+int dev_knob(const char* name, int dflt);
 
 // Records a detail message for ia_last_error() and returns `status`.
 int fail(int status, const char* fmt, ...);

@@ -150,8 +150,19 @@ __global__ void __launch_bounds__(QH_THREADS, 3) quant_heads_kernel(const QHArgs
         if (a.mode == 0) {
           __threadfence();
           atomicAdd(a.count + s, 1);
-          // the team meets here: every CTA of the team is resident (grid <= occupancy)
-          while (*reinterpret_cast<volatile int32_t*>(a.count + s) < T) __nanosleep(128);
+          // The team meets here.  Mode 0 is only ever launched cooperatively
+          // (cudaLaunchAttributeCooperative), so every CTA of the grid is co-resident and
+          // the wait ends; the bound is a second line of defence: after ~2^26 polls
+          // (seconds) the kernel flags IA_QH_ERR_BARRIER and carries on, so the call
+          // fails loudly instead of hanging.
+          uint32_t polls = 0;
+          while (*reinterpret_cast<volatile int32_t*>(a.count + s) < T) {
+            __nanosleep(128);
+            if (++polls == (1u << 26)) {
+              atomicOr(reinterpret_cast<unsigned int*>(a.err), 2u);
+              break;
+            }
+          }
           __threadfence();
         }
         if (a.mode != 1) {
@@ -240,6 +251,30 @@ __global__ void __launch_bounds__(QH_THREADS, 3) quant_heads_kernel(const QHArgs
 
 using namespace ia;
 
+// amax over every slab, then the quantise pass in reverse slab order; no barriers, so
+// the grids need not be resident: ~128 KB of f32 per CTA
+static int quant_heads_split(QHArgs a, void (*kern)(const QHArgs), int64_t grid_max,
+                             int64_t slab_bytes, size_t smem, cudaStream_t stream) {
+  int64_t t2 = (slab_bytes + (128 << 10) - 1) >> 17;
+  t2 = t2 < 1 ? 1 : t2;
+  a.team = (int)t2;
+  a.n_teams = (int)a.n_slabs;
+  // IA_QH_WAVES=w > 0 (profiling build): at most w resident waves of teams, each
+  // striding over slabs
+  static const int waves_env = dev_knob("IA_QH_WAVES", 0);
+  if (waves_env > 0) {
+    const int64_t cap = grid_max * waves_env / t2;
+    if (cap >= 1 && cap < a.n_slabs) a.n_teams = (int)cap;
+  }
+  const uint64_t g2 = (uint64_t)a.n_teams * t2;
+  a.mode = 1;
+  kern<<<(unsigned)g2, QH_THREADS, smem, stream>>>(a);
+  if (int r = check_launch("quant_heads_kernel (amax)")) return r;
+  a.mode = 2;
+  kern<<<(unsigned)g2, QH_THREADS, smem, stream>>>(a);
+  return check_launch("quant_heads_kernel (quantise)");
+}
+
 static int quant_heads_launch(const float* q, const float* k, const float* v, int64_t B,
                               int64_t H, int64_t Hkv, int64_t L, int64_t d,
                               const int32_t* seq_lens, int8_t* qhat, int8_t* khat, int8_t* vt,
@@ -269,7 +304,7 @@ static int quant_heads_launch(const float* q, const float* k, const float* v, in
   a.amax = amax_bits; a.count = counters; a.scales = scales; a.err = err_flag;
   a.n_slabs = B * H + 2 * B * Hkv;
   // V^T block: one 4x4 patch per thread (kb * d_pad = 16 * QH_THREADS bytes)
-  static const int kb_env = getenv("IA_QH_KB") ? atoi(getenv("IA_QH_KB")) : 0;
+  static const int kb_env = dev_knob("IA_QH_KB", 0);
   int kb = (int)(((16 * QH_THREADS) / d_pad) & ~15);
   if (kb_env >= 16 && (kb_env & 15) == 0 && (kb_env / 4) * (d_pad / 4) <= QH_THREADS) kb = kb_env;
   a.kb = kb;
@@ -284,8 +319,8 @@ static int quant_heads_launch(const float* q, const float* k, const float* v, in
   const int64_t slab_bytes = L * d * 4;
   const int64_t slab_elems = L * d;
   // IA_QH_L2MB / IA_QH_TEAM override the L2 budget and team size (A/B runs only)
-  static const int l2mb_env = getenv("IA_QH_L2MB") ? atoi(getenv("IA_QH_L2MB")) : 64;
-  static const int team_env = getenv("IA_QH_TEAM") ? atoi(getenv("IA_QH_TEAM")) : 0;
+  static const int l2mb_env = dev_knob("IA_QH_L2MB", 64);
+  static const int team_env = dev_knob("IA_QH_TEAM", 0);
   int64_t target = ((int64_t)l2mb_env << 20) / (slab_bytes > 0 ? slab_bytes : 1);  // slabs in flight (~64 MB)
   target = target < 1 ? 1 : (target > a.n_slabs ? a.n_slabs : target);
   int64_t team = grid_max / target;
@@ -299,38 +334,34 @@ static int quant_heads_launch(const float* q, const float* k, const float* v, in
   a.team = (int)team;
   a.mode = 0;
   a.per_tensor = per_tensor;
-  static const int pf_env = getenv("IA_QH_PF") ? atoi(getenv("IA_QH_PF")) : 0;
+  static const int pf_env = dev_knob("IA_QH_PF", 0);
   a.pf = pf_env;
   // Many small slabs (C3: 96 x 1 MB) spend more on team barriers than on bytes: run the
   // amax and quantise passes as two barrier-free launches instead (IA_QH_SPLIT=0/1
   // forces either form, for A/B checks).
-  static const int split_env = getenv("IA_QH_SPLIT") ? atoi(getenv("IA_QH_SPLIT")) : -1;
+  static const int split_env = dev_knob("IA_QH_SPLIT", -1);
   // Per-tensor scales need every slab's amax first: always the two-launch form.
   const bool split = per_tensor || (split_env >= 0 ? split_env != 0
                                                    : (slab_bytes <= (1 << 20) && a.n_slabs >= 32));
-  if (split) {
-    // amax over every slab, then the quantise pass in reverse slab order; no barriers,
-    // so the grids need not be resident: ~128 KB of f32 per CTA
-    int64_t t2 = (slab_bytes + (128 << 10) - 1) >> 17;
-    t2 = t2 < 1 ? 1 : t2;
-    a.team = (int)t2;
-    a.n_teams = (int)a.n_slabs;
-    // IA_QH_WAVES=w > 0: at most w resident waves of teams, each striding over slabs
-    static const int waves_env = getenv("IA_QH_WAVES") ? atoi(getenv("IA_QH_WAVES")) : 0;
-    if (waves_env > 0) {
-      const int64_t cap = grid_max * waves_env / t2;
-      if (cap >= 1 && cap < a.n_slabs) a.n_teams = (int)cap;
-    }
-    const uint64_t g2 = (uint64_t)a.n_teams * t2;
-    a.mode = 1;
-    kern<<<(unsigned)g2, QH_THREADS, smem, (cudaStream_t)stream>>>(a);
-    if (int r = check_launch("quant_heads_kernel (amax)")) return r;
-    a.mode = 2;
-    kern<<<(unsigned)g2, QH_THREADS, smem, (cudaStream_t)stream>>>(a);
-    return check_launch("quant_heads_kernel (quantise)");
-  }
-  kern<<<(unsigned)(n_teams * team), QH_THREADS, smem, (cudaStream_t)stream>>>(a);
-  return check_launch("quant_heads_kernel");
+  if (split) return quant_heads_split(a, kern, grid_max, slab_bytes, smem, (cudaStream_t)stream);
+  // Cooperative launch: the runtime guarantees every CTA is co-resident (or refuses the
+  // launch), which is what the team barrier needs -- an occupancy-sized plain launch is
+  // only safe on an otherwise idle device.  If the runtime refuses (kernels on other
+  // streams, MPS / green contexts with fewer SMs), run the barrier-free two-launch form.
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)(n_teams * team));
+  cfg.blockDim = dim3(QH_THREADS);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = (cudaStream_t)stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeCooperative;
+  attr[0].val.cooperative = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  e = cudaLaunchKernelEx(&cfg, kern, a);
+  if (e == cudaSuccess) return check_launch("quant_heads_kernel");
+  (void)cudaGetLastError();  // clear the refused launch; fall back to the split form
+  return quant_heads_split(a, kern, grid_max, slab_bytes, smem, (cudaStream_t)stream);
 }
 
 extern "C" int ia_quant_heads(const float* q, const float* k, const float* v, int64_t B, int64_t H,

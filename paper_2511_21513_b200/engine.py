@@ -121,8 +121,27 @@ def pack_mask(mask: torch.Tensor) -> torch.Tensor:
 
 
 def raise_if_nonfinite(err: torch.Tensor):
-    if int(err.item()) != 0:
+    e = int(err.item())
+    if e & 2:  # quant_heads_kernel: a team barrier timed out (never expected)
+        raise RuntimeError("quantiser team barrier timed out; results discarded")
+    if e != 0:
         raise ValueError("input contains non-finite elements")
+
+
+def check_out(out, q, shape):
+    """A caller-supplied ``out`` is written by the kernel through a raw pointer: it
+    must be a contiguous f32 CUDA tensor of the result's shape on q's device."""
+    if not isinstance(out, torch.Tensor):
+        raise TypeError("out must be a torch.Tensor")
+    if out.device != q.device:
+        raise ValueError(f"out is on {out.device}, the inputs on {q.device}")
+    if out.dtype != torch.float32:
+        raise ValueError(f"out must be float32, got {out.dtype}")
+    if tuple(out.shape) != tuple(shape):
+        raise ValueError(f"out must have shape {tuple(shape)}, got {tuple(out.shape)}")
+    if not out.is_contiguous():
+        raise ValueError("out must be contiguous")
+    return out
 
 
 @dataclass
@@ -275,6 +294,8 @@ def attention(q, k, v, *, causal=False, seq_lens=None, mask=None, scale_granular
         lut = lut_bytes(b, c)
     if out is None:
         out = torch.empty((B, H, Lq, d), dtype=torch.float32, device=q.device)
+    else:
+        check_out(out, q, (B, H, Lq, d))
     if timer is not None:
         timer.mark("start")
     d_pad = pad_head_dim(d)

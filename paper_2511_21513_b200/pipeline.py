@@ -144,14 +144,19 @@ def int_attention(q, k, v, cfg=None, warmup=0, iters=1):
     if k_gran.kind == PER_ROW_GROUP:
         return _int_attention_grouped(qt, kt, vt, mt, cfg, k_gran, lut, numpy_in, warmup, iters)
 
-    _sm._note("logits", np.int32)
-    _sm._note("lut", np.uint8)
-    if mt is not None:
-        _sm._note("mask", np.uint8)
-    _sm._note("prob", np.int8 if cfg.p_format is PFormat.INT8X127 else np.uint8)
-    _sm._note("pv_in", np.int8 if cfg.p_format is PFormat.INT8X127 else np.uint8)
+    p_dt = np.int8 if cfg.p_format is PFormat.INT8X127 else np.uint8
 
     def once(clk):
+        # the reference's per-call audit stream (softmax.py:279-298, pipeline.py:248):
+        # int32 logits (the s32 TMEM accumulator of the QK^T MMA), u8 index map, u8 LUT,
+        # u8 mask, u8 / s8 P^ (the P.V MMA's A operand, in shared memory)
+        _sm._note("logits", np.int32)
+        _sm._note("index_table", np.uint8)
+        _sm._note("lut", lut.entries)
+        if mt is not None:
+            _sm._note("mask", np.uint8)
+        _sm._note("prob", p_dt)
+        _sm._note("pv_in", p_dt)
         return E.attention(qt[None, None], kt[None, None], vt[None, None], mask=mt,
                            b=cfg.b, c=cfg.c, p_scale=p_scale, lut=lut.entries, timer=clk)
 
@@ -188,7 +193,7 @@ def _int_attention_grouped(qt, kt, vt, mt, cfg, k_gran, lut, numpy_in, warmup, i
                                          p_format=cfg.p_format)
         if clk:
             clk.mark("softmax")
-        _sm._note("pv_in", np.int8 if cfg.p_format is PFormat.INT8X127 else np.uint8)
+        _sm._note("pv_in", prob.values)
         acc = gemm_pv(prob.values, vh)
         if clk:
             clk.mark("pv")

@@ -3,16 +3,20 @@
 Every (b, KV head) group -- its KV head plus the H/Hkv query heads that read it
 -- is independent: row max, row sum and normalisation are per query row, so
 there is no inter-GPU reduction in per-head scale mode.  The
-launcher therefore
+reference has no multi-head loop at all (SPEC.md:344 leaves it to the caller);
+this launcher is that loop spread over one process per GPU:
 
-  * plans which groups each rank owns (contiguous KV-head groups, or LPT --
-    longest processing time first -- over causal/varlen costs, as config 5
-    needs),
-  * runs each rank's groups with the fused kernel on its own GPU (one process
-    per GPU, ``torch.distributed`` over NCCL),
-  * uses a collective only where the path has a real exchange: an
+  * ``plan`` decides which groups each rank owns (contiguous KV-head groups, or
+    LPT -- longest processing time first -- over causal / varlen costs, as
+    config 5 needs);
+  * ``pack`` gathers a rank's groups into contiguous [n, g, L, d] / [n, 1, L, d]
+    blocks (on the device when the inputs are CUDA tensors);
+  * each rank runs its groups through the fused kernel on its own GPU;
+  * a collective runs only where the path has a real exchange: an
     all-reduce(MAX) of the three global amax values in ``scale_granularity=
-    "tensor"`` mode, and an optional gather of the f32 outputs.
+    "tensor"`` mode, and the gather of the f32 outputs when the caller wants
+    them on one device.  Under NCCL both run on the rank's CUDA device (NVLink);
+    under gloo (CPU tests) on the host.
 
 The per-rank compute is injectable (``compute=``) so the host logic -- plan,
 pack, global-scale exchange, gather -- is testable on CPU with ``gloo``.
@@ -86,43 +90,143 @@ def plan(B, H, Hkv, L, world, *, lens=None, causal=False, policy="auto"):
 
 
 def pack(q, k, v, groups, g, lens=None):
-    """Gather the groups' slices into contiguous [n, g, L, d] / [n, 1, L, d] arrays."""
-    idx_b = [gr.b for gr in groups]
-    qs = np.stack([q[gr.b, gr.kvh * g:(gr.kvh + 1) * g] for gr in groups]) if groups else None
-    ks = np.stack([k[gr.b, gr.kvh:gr.kvh + 1] for gr in groups]) if groups else None
-    vs = np.stack([v[gr.b, gr.kvh:gr.kvh + 1] for gr in groups]) if groups else None
-    sl = None if lens is None else np.asarray([lens[b] for b in idx_b], np.int32)
+    """Gather the groups' slices into contiguous [n, g, L, d] / [n, 1, L, d] blocks
+    (numpy in -> numpy out; torch in -> torch out on the same device) plus the
+    per-group valid lengths (int32 numpy, or None)."""
+    if not groups:
+        return None, None, None, None
+    stack = torch.stack if isinstance(q, torch.Tensor) else np.stack
+    qs = stack([q[gr.b, gr.kvh * g:(gr.kvh + 1) * g] for gr in groups])
+    ks = stack([k[gr.b, gr.kvh:gr.kvh + 1] for gr in groups])
+    vs = stack([v[gr.b, gr.kvh:gr.kvh + 1] for gr in groups])
+    sl = None if lens is None else np.asarray([lens[gr.b] for gr in groups], np.int32)
     return qs, ks, vs, sl
 
 
+def collective_device(group=None) -> torch.device:
+    """Where this process group's collectives run: the rank's CUDA device under
+    NCCL (NVLink / NVSwitch), the host under gloo."""
+    if dist.is_initialized() and dist.get_backend(group) == "nccl":
+        return torch.device("cuda", torch.cuda.current_device())
+    return torch.device("cpu")
+
+
 def _default_compute(qs, ks, vs, *, causal, seq_lens, scale_granularity, cfg, scales):
+    """The rank's groups through the fused kernel.  CUDA tensors in -> CUDA tensor
+    out (no host round trip); host arrays are copied to the device and the result
+    copied back."""
     from . import engine as E
     dev = torch.device("cuda", torch.cuda.current_device())
-    qt, kt, vt = (torch.from_numpy(np.ascontiguousarray(x)).to(dev) for x in (qs, ks, vs))
-    sl = None if seq_lens is None else torch.from_numpy(seq_lens).to(dev)
-    sc = None if scales is None else tuple(torch.tensor([s], dtype=torch.float32, device=dev)
-                                           for s in scales)
+    on_dev = isinstance(qs, torch.Tensor) and qs.is_cuda
+    if on_dev:
+        qt, kt, vt = (x.contiguous() for x in (qs, ks, vs))
+    else:
+        qt, kt, vt = (torch.as_tensor(np.ascontiguousarray(x)).to(dev) for x in (qs, ks, vs))
+    sl = None if seq_lens is None else torch.as_tensor(seq_lens, dtype=torch.int32).to(dev)
+    sc = None
+    if scales is not None:
+        sc = tuple(s.reshape(1).to(dev, torch.float32) if isinstance(s, torch.Tensor)
+                   else torch.tensor([s], dtype=torch.float32, device=dev) for s in scales)
     out = E.attention(qt, kt, vt, causal=causal, seq_lens=sl, scale_granularity=scale_granularity,
                       b=cfg.b, c=cfg.c, p_scale=cfg.p_format.value, scales=sc)
-    return out.cpu().numpy()
+    return out if on_dev else out.cpu().numpy()
 
 
-def _local_amax(x, lens_per_group=None):
-    a = np.abs(x)
-    if not np.isfinite(a).all():
-        raise ValueError("input contains non-finite elements")
-    return np.float32(a.max()) if a.size else np.float32(0)
+def _local_amax_host(x, sl):
+    """Exact max|x| over each packed group's valid rows (host arrays)."""
+    best = np.float32(0)
+    for u in range(x.shape[0]):
+        rows = x[u] if sl is None else x[u, :, :int(sl[u])]
+        a = np.abs(np.asarray(rows))
+        if not np.isfinite(a).all():
+            raise ValueError("input contains non-finite elements")
+        if a.size:
+            best = max(best, np.float32(a.max()))
+    return best
+
+
+def _local_amax_device(x, sl):
+    """max|x| over the valid rows of every packed group with the library's amax
+    kernel (float bits, exact); returns a 1-element f32 CUDA tensor."""
+    from . import engine as E
+    n, g, L, d = x.shape
+    buf = torch.zeros(2, dtype=torch.int32, device=x.device)
+    slt = None if sl is None else torch.as_tensor(sl, dtype=torch.int32).to(x.device)
+    E.amax_rows(x.contiguous(), n * g, L, d, buf[:1], buf[1:], seq_lens=slt, valid_div=g,
+                slot_div=n * g)
+    E.raise_if_nonfinite(buf[1:])
+    return buf[:1].view(torch.float32)
+
+
+def global_scales(qs, ks, vs, sl, group=None, world=1):
+    """Global per-tensor scales of a sharded batch: every rank contributes the amax
+    of the rows it owns, all-reduce(MAX) of 3 floats on the collective device, then
+    s = max(amax, 1e-12) / 127 in f32 (quantize.py:113).  Returns 3 f32 scales
+    (numpy scalars)."""
+    cdev = collective_device(group)
+    if qs is None:
+        local = torch.zeros(3, dtype=torch.float32)
+    elif isinstance(qs, torch.Tensor) and qs.is_cuda:
+        local = torch.cat([_local_amax_device(x, sl) for x in (qs, ks, vs)])
+    else:
+        local = torch.tensor([_local_amax_host(x, sl) for x in (qs, ks, vs)], dtype=torch.float32)
+    local = local.to(cdev)
+    if world > 1:
+        dist.all_reduce(local, op=dist.ReduceOp.MAX, group=group)
+    amax = local.cpu().numpy()
+    return tuple(np.float32(np.maximum(a, np.float32(1e-12)) / np.float32(127)) for a in amax)
+
+
+def gather_blocks(local_out, ranks, rank, shape, g, *, group=None, gather_to=0, like=None):
+    """Gather every rank's packed [n_r, g, L, d] block into the full [B, H, L, d]
+    output.  ``gather_to`` = a rank (dist.gather: only that rank receives, the
+    NVLink traffic is (world - 1) blocks) or "all" (all_gather_into_tensor).  The
+    full output is a CUDA tensor on the collective device under NCCL, else numpy
+    (or a CPU tensor when ``like`` is a tensor); ranks that do not receive get None.
+    """
+    B, H, L, d = shape
+    world = len(ranks)
+    G = g
+    cdev = collective_device(group)
+    max_n = max(len(r) for r in ranks)
+    blk = torch.zeros((max_n, G, L, d), dtype=torch.float32, device=cdev)
+    if local_out is not None:
+        src = local_out if isinstance(local_out, torch.Tensor) else torch.from_numpy(
+            np.ascontiguousarray(local_out))
+        blk[:src.shape[0]].copy_(src.to(cdev, non_blocking=True))
+    if world == 1:
+        parts = [blk]
+    elif gather_to == "all":
+        big = torch.empty((world * max_n, G, L, d), dtype=torch.float32, device=cdev)
+        dist.all_gather_into_tensor(big, blk, group=group) if cdev.type == "cuda" else \
+            dist.all_gather(list(big.chunk(world)), blk, group=group)
+        parts = list(big.chunk(world))
+    else:
+        recv = rank == gather_to
+        parts = [torch.empty_like(blk) for _ in range(world)] if recv else None
+        dist.gather(blk, parts, dst=gather_to, group=group)
+        if not recv:
+            return None
+    out = torch.empty((B, H, L, d), dtype=torch.float32, device=cdev)
+    for r, grs in enumerate(ranks):
+        for u, gr in enumerate(grs):
+            out[gr.b, gr.kvh * G:(gr.kvh + 1) * G] = parts[r][u]
+    if cdev.type == "cuda" or isinstance(like, torch.Tensor):
+        return out
+    return out.numpy()
 
 
 def sharded_attention(q, k, v, *, causal=False, seq_lens=None, scale_granularity="head",
-                      cfg=None, group=None, gather_to=0, policy="auto", compute=None,
-                      amax_device=None):
+                      cfg=None, group=None, gather_to=0, policy="auto", compute=None):
     """Run this rank's share of a batched IntAttention and (optionally) gather.
 
-    Every rank passes the same full host arrays q [B,H,L,d], k/v [B,Hkv,L,d].
-    Returns (out, groups): ``out`` is the full [B,H,L,d] f32 result on rank
-    ``gather_to`` (None elsewhere) when gather_to is not None, else this rank's
-    packed [n, g, L, d] block; ``groups`` lists this rank's (b, kvh) groups.
+    Every rank passes the same full q [B,H,L,d], k/v [B,Hkv,L,d]: host arrays, or
+    CUDA tensors on the rank's device (then packing, compute and collectives stay
+    on the device).  Returns (out, groups): with ``gather_to`` a rank (default 0)
+    or "all", ``out`` is the full [B,H,L,d] f32 result on the receiving rank(s)
+    (a CUDA tensor under NCCL / for CUDA inputs, numpy for host inputs under gloo;
+    None elsewhere); with ``gather_to=None`` it is this rank's packed [n, g, L, d]
+    block.  ``groups`` lists this rank's (b, kvh) groups.
     """
     from .pipeline import AttentionConfig
     cfg = cfg or AttentionConfig()
@@ -131,29 +235,15 @@ def sharded_attention(q, k, v, *, causal=False, seq_lens=None, scale_granularity
     B, H, L, d = q.shape
     Hkv = k.shape[1]
     g = H // Hkv
-    lens = None if seq_lens is None else np.asarray(seq_lens, np.int64)
+    lens = None if seq_lens is None else np.asarray(
+        seq_lens.cpu() if isinstance(seq_lens, torch.Tensor) else seq_lens, np.int64)
     ranks = plan(B, H, Hkv, L, world, lens=lens, causal=causal, policy=policy)
     mine = ranks[rank]
     qs, ks, vs, sl = pack(q, k, v, mine, g, lens)
 
     scales = None
     if scale_granularity == "tensor":
-        # one global scale per tensor: every rank contributes the amax of the rows
-        # it owns; all-reduce(MAX) of 3 floats
-        local = np.zeros(3, np.float32)
-        if mine:
-            for t, x in enumerate((qs, ks, vs)):
-                if sl is None:
-                    local[t] = _local_amax(x)
-                else:
-                    local[t] = max((_local_amax(x[u, :, :sl[u]]) for u in range(len(mine))),
-                                   default=np.float32(0))
-        dev = amax_device or torch.device("cpu")
-        tl = torch.from_numpy(local).to(dev)
-        if world > 1:
-            dist.all_reduce(tl, op=dist.ReduceOp.MAX, group=group)
-        amax = tl.cpu().numpy()
-        scales = tuple(np.float32(np.maximum(a, np.float32(1e-12)) / np.float32(127)) for a in amax)
+        scales = global_scales(qs, ks, vs, sl, group=group, world=world)
 
     fn = compute or _default_compute
     local_out = None
@@ -162,24 +252,8 @@ def sharded_attention(q, k, v, *, causal=False, seq_lens=None, scale_granularity
                        cfg=cfg, scales=scales)
     if gather_to is None:
         return local_out, mine
-
-    # gather: pad every rank's block to the largest group count
-    max_n = max(len(r) for r in ranks)
-    buf = np.zeros((max_n, g, L, d), np.float32)
-    if mine:
-        buf[:len(mine)] = local_out
-    dev = amax_device or torch.device("cpu")
-    t = torch.from_numpy(buf).to(dev)
-    if world > 1:
-        parts = [torch.empty_like(t) for _ in range(world)]
-        dist.all_gather(parts, t, group=group)
-    else:
-        parts = [t]
-    if rank != gather_to:
-        return None, mine
-    out = np.zeros((B, H, L, d), np.float32)
-    for r, grs in enumerate(ranks):
-        blk = parts[r].cpu().numpy()
-        for u, gr in enumerate(grs):
-            out[gr.b, gr.kvh * g:(gr.kvh + 1) * g] = blk[u]
+    out = gather_blocks(local_out, ranks, rank, (B, H, L, d), g, group=group,
+                        gather_to=gather_to, like=q)
+    if out is not None and isinstance(q, torch.Tensor) and q.is_cuda and out.device != q.device:
+        out = out.to(q.device)
     return out, mine

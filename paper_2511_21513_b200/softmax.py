@@ -92,8 +92,11 @@ _audit_sink = None
 @contextlib.contextmanager
 def dataflow_audit(sink):
     """Collect (tag, dtype) records of tensors crossing the softmax stage
-    (softmax.py:207-228).  For the fused kernel the records are the dtypes of
-    its on-chip stage buffers: int32 logits (TMEM), uint8 LUT, uint8 P^."""
+    (softmax.py:207-228), in the reference's order: logits, index_table, lut,
+    [mask], prob (+ pv_in from int_attention, pipeline.py:248); grouped:
+    surrogates, prob.  For the fused kernel the logits / prob / pv_in records are
+    the dtypes its instruction encodings fix for the on-chip buffers (s32 TMEM
+    accumulator of tcgen05.mma kind::i8; u8 / s8 A operand of the P.V MMA)."""
     global _audit_sink
     prev = _audit_sink
     _audit_sink = sink
@@ -103,9 +106,22 @@ def dataflow_audit(sink):
         _audit_sink = prev
 
 
-def _note(tag, dtype):
+_TORCH_NP = {torch.int32: np.int32, torch.uint8: np.uint8, torch.int8: np.int8,
+             torch.int64: np.int64, torch.float32: np.float32}
+
+
+def _note(tag, x):
+    """Record (tag, dtype) of ``x``: an observed array / tensor, or -- for a buffer
+    that lives only on chip inside the fused kernel (TMEM logits, smem P^) -- the
+    dtype the kernel's instruction encoding fixes for it."""
     if _audit_sink is not None:
-        _audit_sink.append((tag, np.dtype(dtype)))
+        if isinstance(x, torch.Tensor):
+            dt = np.dtype(_TORCH_NP[x.dtype])
+        elif isinstance(x, np.ndarray):
+            dt = x.dtype
+        else:
+            dt = np.dtype(x)
+        _audit_sink.append((tag, dt))
 
 
 def _check_lut(lut):
@@ -148,19 +164,20 @@ def index_softmax(logits, c_int, lut, mask=None, p_format=PFormat.UINT8X255, thr
         raise ValueError("c_int must be >= 1")
     ci = min(ci, _C_INT_CAP)
     numpy_in = not is_torch(values)
-    _note("logits", np.int32)
-    _note("lut", np.uint8)
     lv = to_device(values, np.int32)
+    _note("logits", lv)
+    # the reference's u8 index table (softmax.py:124-128, :280-282) is an exact
+    # magic-number division here (csrc/params.cuh); its entries are u8 indices
+    _note("index_table", np.uint8)
+    _note("lut", lut.entries)
     m = None
     if mask is not None:
         m = _prep_mask(mask, lv.shape)
-        _note("mask", np.uint8)
+        _note("mask", np.uint8)  # staged as u8, then bit-packed (engine.pack_mask)
     out = E.index_softmax_dev(lv, ci, lut.entries, m, p_format.value)
     if p_format is PFormat.INT8X127:
         out = out.view(torch.int8)
-        _note("prob", np.int8)
-    else:
-        _note("prob", np.uint8)
+    _note("prob", out)
     return ProbMatrix(values=to_host(out, numpy_in), denom_scale=p_format.value)
 
 

@@ -164,7 +164,23 @@ def make_c5(seed: int = 0) -> Workload:
     return Workload("C5", q, k, v, causal=True, seq_lens=lens.astype(np.int32))
 
 
-MAKERS = {"C1": make_c1, "C2": make_c2, "C3": make_c3, "C4": make_c4, "C5": make_c5}
+def make_tiny(seed: int = 0) -> Workload:
+    """Not a BASELINE config: a seconds-sized GQA + varlen causal batch for the CPU
+    (gloo) test of bench.py's multi-rank path."""
+    B, H, Hkv, d = 3, 4, 2, 32
+    rng = np.random.default_rng(seed)
+    lens = rng.integers(40, 96, size=B, endpoint=True)
+    L = int(lens.max())
+    q = rng.standard_normal((B, H, L, d), dtype=np.float32)
+    k = rng.standard_normal((B, Hkv, L, d), dtype=np.float32)
+    v = rng.standard_normal((B, Hkv, L, d), dtype=np.float32)
+    for b, n in enumerate(lens):
+        q[b, :, n:] = k[b, :, n:] = v[b, :, n:] = 0
+    return Workload("tiny", q, k, v, causal=True, seq_lens=lens.astype(np.int32))
+
+
+MAKERS = {"C1": make_c1, "C2": make_c2, "C3": make_c3, "C4": make_c4, "C5": make_c5,
+          "tiny": make_tiny}
 
 
 def make(name: str, seed: int = 0) -> Workload:

@@ -167,3 +167,56 @@ def run_error_case(fn, m):
     except Exception as e:  # noqa: BLE001
         return type(e).__name__
     return "ok"
+
+
+def audit_cases():
+    """Calls whose ``dataflow_audit`` tag stream is pinned against the reference
+    (softmax.py:207-228; notes at softmax.py:279-298, :394-398, pipeline.py:248).
+    name -> fn(m) running the call on module ``m`` (the reference ``intattn`` or
+    ``paper_2511_21513_b200``); the harness wraps it in ``m.dataflow_audit``."""
+    rng = np.random.default_rng(777)
+    L, d = 48, 32
+    q, k, v = (rng.standard_normal((L, d), dtype=np.float32) for _ in range(3))
+    causal = np.triu(np.ones((L, L), bool), 1)
+    logits = rng.integers(-5000, 5000, size=(L, L), dtype=np.int32)
+
+    def attn(**kw):
+        def fn(m):
+            cfg = m.AttentionConfig(**{key: (val(m) if callable(val) else val)
+                                       for key, val in kw.items() if key not in ("warmup", "iters")})
+            m.int_attention(q, k, v, cfg, warmup=kw.get("warmup", 0), iters=kw.get("iters", 1))
+        return fn
+
+    def isoft(mask=None, p127=False):
+        def fn(m):
+            fmt = m.PFormat.INT8X127 if p127 else m.PFormat.UINT8X255
+            m.index_softmax(logits, m.ClipThreshold(c_int=4000), m.build_lut(5, 6.6), mask=mask,
+                            p_format=fmt)
+        return fn
+
+    def grouped(m):
+        groups = np.repeat(np.arange(3), L // 3)
+        m.index_softmax_grouped(logits, groups, [0.002, 0.001, 0.004], 6.6, m.build_lut(5, 6.6),
+                                mask=causal)
+
+    def qonly(m):
+        m.quant_only_attention(q, k, v)
+
+    return {
+        "int_attention": attn(),
+        "int_attention_warmup1_iters2": attn(warmup=1, iters=2),
+        "int_attention_causal_mask": attn(mask=causal),
+        "int_attention_int8x127": attn(p_format=lambda m: m.PFormat.INT8X127),
+        "int_attention_row_group_k": attn(granularity=lambda m: m.QuantGranularity.per_row_group(16)),
+        "index_softmax": isoft(),
+        "index_softmax_mask_int8x127": isoft(mask=causal, p127=True),
+        "index_softmax_grouped": grouped,
+        "quant_only_attention": qonly,
+    }
+
+
+def run_audit_case(fn, m):
+    sink = []
+    with m.dataflow_audit(sink):
+        fn(m)
+    return [[tag, np.dtype(dt).str] for tag, dt in sink]

@@ -25,3 +25,21 @@ def configs():
 
 def f32(h):
     return np.float32(float.fromhex(h))
+
+
+def unit_mismatches(out, wl, name):
+    """(b, h) units of a [B, H, L, d] f32 output whose valid rows do not hash to the
+    live reference's digest in configs.json (or whose padding rows are not +0.0).
+    Returns (bad units, units checked); raises KeyError if the config has no golden."""
+    from cases import digest
+    G = configs()[name]
+    B, H = out.shape[:2]
+    lens = wl.lengths()
+    bad, u = [], 0
+    for b in range(B):
+        for h in range(H):
+            n = int(lens[b])
+            if digest(out[b, h, :n]) != G["unit_digests"][u] or out[b, h, n:].view(np.uint32).any():
+                bad.append((b, h))
+            u += 1
+    return bad, u

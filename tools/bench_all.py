@@ -71,7 +71,8 @@ def run(name, iters, softmax="index"):
                 u += 1
         exact = bad == 0
     ops = wl.ops()
-    qbytes = 5 * (wl.q.size + wl.k.size + wl.v.size)
+    # algorithmic quantiser bytes over VALID rows only (pad rows are never read)
+    qbytes = 5 * int(wl.lengths().sum()) * (H + 2 * Hkv) * d
     return {"config": name, "softmax": softmax, "shape": [B, H, Hkv, L, d], "causal": wl.causal, "scale": gran,
             "ms_total": tot * 1e3, "ms_quantize": qnt * 1e3, "ms_fused": att * 1e3,
             "tops_total": ops / tot / 1e12, "tops_fused": ops / att / 1e12,
