@@ -193,7 +193,9 @@ def gather_blocks(local_out, ranks, rank, shape, g, *, group=None, gather_to=0, 
     if local_out is not None:
         src = local_out if isinstance(local_out, torch.Tensor) else torch.from_numpy(
             np.ascontiguousarray(local_out))
-        blk[:src.shape[0]].copy_(src.to(cdev, non_blocking=True))
+        # device -> device stays stream-ordered; device -> host must be a blocking copy
+        # (a non_blocking D2H returns before the bytes have landed)
+        blk[:src.shape[0]].copy_(src, non_blocking=cdev.type == "cuda" and src.is_cuda)
     if world == 1:
         parts = [blk]
     elif gather_to == "all":
