@@ -31,6 +31,7 @@
 #include <cstdint>
 #include <cstdlib>
 #include <cstring>
+#include <type_traits>
 
 #include "common.cuh"
 #include "params.cuh"
@@ -105,7 +106,7 @@ struct Cfg {
 // For nlut <= 32 the u32 table is zero-extended to 56 entries so warps whose
 // largest reachable index is < 56 can skip the per-logit clip (IdxMap::idx_u).
 __host__ __device__ constexpr bool wide_tab(int nlut) { return nlut <= 64; }
-__host__ __device__ constexpr int tab_entries(int nlut) { return nlut <= 32 ? 56 : nlut; }
+__host__ __device__ constexpr int tab_entries(int nlut) { return row_table_entries(nlut); }
 
 template <int DP>
 constexpr size_t attn_smem_bytes(int nlut) {
@@ -127,6 +128,14 @@ __device__ __forceinline__ uint32_t lds_u8(uint32_t addr) {
   uint32_t v;
   asm("ld.shared.u8 %0, [%1];" : "=r"(v) : "r"(addr));
   return v;
+}
+// (a & b) | c as one LOP3 the compiler cannot re-associate: the row-table address
+// (umulhi(n, magic9) & ~511) | row*4 then joins the table base inside the LDS
+// ([R + UR + imm] addressing) instead of costing an extra IADD per logit.
+__device__ __forceinline__ uint32_t and_or(uint32_t a, uint32_t b, uint32_t c) {
+  uint32_t r;
+  asm("lop3.b32 %0, %1, %2, %3, 0xEA;" : "=r"(r) : "r"(a), "r"(b), "r"(c));  // (a & b) | c
+  return r;
 }
 __device__ __forceinline__ uint32_t lds_u32(uint32_t addr) {
   uint32_t v;
@@ -174,6 +183,27 @@ __device__ __forceinline__ void bwait(uint64_t* bar, uint32_t parity, bool spin)
   if (spin) mbar_wait_spin(bar, parity);
   else mbar_wait(bar, parity);
 }
+// Layout / wait-policy variants (A/B builds):
+//   IA_ROLE_FIRST          role warps at warp ids 0-3 (lowest arbitration priority)
+//   IA_PRODUCER_BACKOFF_NS TMA producers poll with a fixed back-off (0: suspended try_wait)
+//   IA_ISSUER_BACKOFF_NS   MMA issuers likewise
+#ifndef IA_ROLE_FIRST
+#define IA_ROLE_FIRST 0
+#endif
+#ifndef IA_PRODUCER_BACKOFF_NS
+#define IA_PRODUCER_BACKOFF_NS 0
+#endif
+#ifndef IA_ISSUER_BACKOFF_NS
+#define IA_ISSUER_BACKOFF_NS 0
+#endif
+__device__ __forceinline__ void pwait(uint64_t* bar, uint32_t parity, bool spin) {
+  if (IA_PRODUCER_BACKOFF_NS > 0 && !spin) mbar_wait_backoff(bar, parity, IA_PRODUCER_BACKOFF_NS);
+  else bwait(bar, parity, spin);
+}
+__device__ __forceinline__ void iwait(uint64_t* bar, uint32_t parity, bool spin) {
+  if (IA_ISSUER_BACKOFF_NS > 0 && !spin) mbar_wait_backoff(bar, parity, IA_ISSUER_BACKOFF_NS);
+  else bwait(bar, parity, spin);
+}
 
 template <int DP, bool DEBUG, bool SKEL = false, bool QO = false>
 __global__ void __launch_bounds__(Cfg<DP>::NTHREADS, 1)
@@ -218,7 +248,10 @@ __global__ void __launch_bounds__(Cfg<DP>::NTHREADS, 1)
   // warp scheduler favours the highest warp id among eligible warps, so the
   // latency-critical TMA / MMA issue loops win their issue slots over the
   // arithmetic-heavy softmax warps sharing their SM sub-partition.
-  const int rw = warp - 4 * NWG;  // role: 0 K producer, 1 QK^T, 2 V^T producer + TMEM alloc, 3 P.V
+  // role: 0 K producer, 1 QK^T, 2 V^T producer + TMEM alloc, 3 P.V; < 0: softmax warp
+  const int rw = IA_ROLE_FIRST ? (warp < 4 ? warp : -1) : warp - 4 * NWG;
+  const int sw = IA_ROLE_FIRST ? warp - 4 : warp;  // softmax warp index (when rw < 0)
+  const int stid = IA_ROLE_FIRST ? (int)threadIdx.x - 128 : (int)threadIdx.x;
 
   if (q0 >= len) {  // the whole query tile is padding: +0.0 rows (pipeline contract)
     const int rows = min(BM, p.L - q0);
@@ -226,7 +259,7 @@ __global__ void __launch_bounds__(Cfg<DP>::NTHREADS, 1)
     for (int t = threadIdx.x; t < rows * p.d; t += C::NTHREADS) o[t] = 0.0f;
     return;
   }
-  if (threadIdx.x == 128 * NWG) IA_TMARK(6);
+  if (rw == 0 && lane == 0) IA_TMARK(6);
   const int key_end = p.causal ? min(q0 + BM, len) : len;
   const int n_kt = (key_end + BN - 1) / BN;
   const bool resident = n_kt <= NWG;  // every logit tile fits its own TMEM buffer
@@ -289,7 +322,7 @@ __global__ void __launch_bounds__(Cfg<DP>::NTHREADS, 1)
     const int t3 = PV_PASS * n_kt;
     const int nloads = npass * n_kt;
     for (int t = 0; t < nloads; ++t) {
-      bwait(k_empty + ks, ((kph >> ks) & 1u) ^ 1u, XF(16));
+      pwait(k_empty + ks, ((kph >> ks) & 1u) ^ 1u, XF(16));
       kph ^= 1u << ks;
       if (elect_one()) {
         IA_TRACE(0, 1, t);
@@ -308,7 +341,7 @@ __global__ void __launch_bounds__(Cfg<DP>::NTHREADS, 1)
     // ------------------------------------------------------------ V^T producer
     int vs = 0, vph = 0;
     for (int n = 0; n < n_kt_b; ++n) {
-      bwait(v_empty + vs, vph ^ 1, XF(16));
+      pwait(v_empty + vs, vph ^ 1, XF(16));
       if (elect_one()) {
         IA_TRACE(2, 5, n);
         mbar_expect_tx(v_full + vs, C::V_BYTES);
@@ -336,12 +369,12 @@ __global__ void __launch_bounds__(Cfg<DP>::NTHREADS, 1)
       const bool need_free = (used >> w) & 1u;
       const uint32_t f_ok = need_free ? mbar_test(s_free + w, (c_s >> w) & 1u) : 1u;
       const uint32_t k_ok = mbar_test(k_full + ks, (kph >> ks) & 1u);
-      if (!f_ok) bwait(s_free + w, (c_s >> w) & 1u, XF(2));
+      if (!f_ok) iwait(s_free + w, (c_s >> w) & 1u, XF(2));
       if (need_free) c_s ^= 1u << w;
       used |= 1u << w;
       if (lane == 0) IA_TRACE(1, 5, t);
       long long t1 = clk64();
-      if (!k_ok) bwait(k_full + ks, (kph >> ks) & 1u, XF(2));
+      if (!k_ok) iwait(k_full + ks, (kph >> ks) & 1u, XF(2));
       kph ^= 1u << ks;
       long long t2 = clk64();
       IA_TADD(8, t1 - t0);
@@ -376,9 +409,9 @@ __global__ void __launch_bounds__(Cfg<DP>::NTHREADS, 1)
     for (int n = 0; n < n_kt_b; ++n) {
       const int pb = w * C::NPB + tl % C::NPB;
       long long t0 = clk64();
-      bwait(p_full + pb, (uint32_t)(tl / C::NPB) & 1u, XF(8));
+      iwait(p_full + pb, (uint32_t)(tl / C::NPB) & 1u, XF(8));
       long long t1 = clk64();
-      bwait(v_full + vs, vph, XF(8));
+      iwait(v_full + vs, vph, XF(8));
       long long t2 = clk64();
       IA_TADD(11, t1 - t0);
       IA_TADD(12, t2 - t1);
@@ -401,7 +434,7 @@ __global__ void __launch_bounds__(Cfg<DP>::NTHREADS, 1)
     __syncwarp();
   } else if (rw < 0) {
     // ------------------------------------------------------------ IndexSoftmax warpgroups
-    const int wg = warp >> 2;
+    const int wg = sw >> 2;
     const int quad = warp & 3;  // TMEM lane quadrant accessible to this warp
     const int row = quad * 32 + lane;
     const int i = q0 + row;
@@ -417,7 +450,7 @@ __global__ void __launch_bounds__(Cfg<DP>::NTHREADS, 1)
     // Each tile is read from TMEM in two 64-column batches (two x32 loads in
     // flight per wait); S[w] is handed back to the MMA warp right after the last
     // load of the tile, in every pass.
-    const bool tm = (threadIdx.x == 0);
+    const bool tm = (stid == 0);
     const bool trw = IA_PROFILE && lane == 0;  // one trace segment per softmax warp
     if (tm) IA_TMARK(0);
     // ---- pass 1: row max over unmasked keys (softmax.py:139-143, :174-179); the row
@@ -432,7 +465,7 @@ __global__ void __launch_bounds__(Cfg<DP>::NTHREADS, 1)
     for (int n = wg; n < n_kt; n += NWG) {
       long long tw0 = clk64();
       bwait(s_full + wg, s_ph, XF(4));
-      if (trw) IA_TRACE(4 + warp, 8, 0 * n_kt + n);
+      if (trw) IA_TRACE(4 + sw, 8, 0 * n_kt + n);
       s_ph ^= 1u;
       if (tm) IA_TADD(15, clk64() - tw0);
       tc_fence_after();
@@ -444,7 +477,7 @@ __global__ void __launch_bounds__(Cfg<DP>::NTHREADS, 1)
           tc_fence_before();
           __syncwarp();
           if (lane == 0) mbar_arrive(s_free + wg);
-          if (trw) IA_TRACE(4 + warp, 9, 0 * n_kt + n);
+          if (trw) IA_TRACE(4 + sw, 9, 0 * n_kt + n);
         }
         const int j0 = n * BN + hb * 64;
         if (DEBUG && p.dbg_logits && i < p.L) {
@@ -568,7 +601,7 @@ __global__ void __launch_bounds__(Cfg<DP>::NTHREADS, 1)
       if (!resident) {
         long long tw0 = clk64();
         bwait(s_full + wg, s_ph, XF(4));
-        if (trw) IA_TRACE(4 + warp, 8, 1 * n_kt + n);
+        if (trw) IA_TRACE(4 + sw, 8, 1 * n_kt + n);
         s_ph ^= 1u;
         if (tm) IA_TADD(14, clk64() - tw0);
       }
@@ -581,7 +614,7 @@ __global__ void __launch_bounds__(Cfg<DP>::NTHREADS, 1)
           tc_fence_before();
           __syncwarp();
           if (lane == 0) mbar_arrive(s_free + wg);
-          if (trw) IA_TRACE(4 + warp, 9, 1 * n_kt + n);
+          if (trw) IA_TRACE(4 + sw, 9, 1 * n_kt + n);
         }
         if (SKEL) continue;
         const int j0 = n * BN + hb * 64;
@@ -652,6 +685,25 @@ __global__ void __launch_bounds__(Cfg<DP>::NTHREADS, 1)
     const uint32_t tab_sh = wtab ? 9u : 7u;
     const uint32_t tab0 = smem_u32(tab), row4 = (uint32_t)row * 4u;
     const uint32_t m9 = (wtab && !(XF(256))) ? hp.magic9 : 0u;
+    // Row threshold of the pass-3 group skip: P^ = rowtab[idx] > 0 only for idx <= t*,
+    // t* = max{t : 2*scale*lut[t] >= S} (rowtab[t] = (2 scale lut[t] + S) // 2S), i.e.
+    // only for delta < T = ceil(c_eff (2t* + 1) / 2k) (idx(delta) > t* from there on),
+    // i.e. only for logits a >= theta = m - T + 1.  A group of keys whose largest logit
+    // is below theta in every row of the warp is all zero.  Scans every LUT entry, so
+    // it holds for any LUT (no monotonicity assumed).
+    // Only rows long enough for P^ to be sparse pay the per-row scan (n_kt >= 16);
+    // shorter rows keep theta = INT_MIN (no group is skipped).
+    int32_t theta = n_kt >= 16 ? INT_MAX : INT_MIN;
+    if (!QO && m9 && n_kt >= 16 && row_valid && !dead && S) {
+      int tstar = -1;
+      for (int t = 0; t < nlut; ++t)
+        if ((uint32_t)p.scale_x2 * (uint32_t)lut8[t] >= S) tstar = t;
+      if (tstar >= 0) {
+        const int64_t T = (hp.c_eff * (2 * (int64_t)tstar + 1) + 2 * (int64_t)k - 1) / (2 * (int64_t)k);
+        const int64_t th = (int64_t)m - T + 1;
+        theta = th < (int64_t)INT_MIN ? INT_MIN : (th > (int64_t)INT_MAX ? INT_MAX : (int32_t)th);
+      }
+    }
     // this thread's row of its warpgroup's P^ tile (K-major, 128B swizzle: 16-byte
     // unit x of row r lives at unit x ^ (r % 8))
     const uint32_t p_rows = smem_u32(smem + C::OFF_P + wg * C::NPB * C::P_BYTES) + (uint32_t)row * 128;
@@ -663,7 +715,7 @@ __global__ void __launch_bounds__(Cfg<DP>::NTHREADS, 1)
       if (!resident) {
         long long tw0 = clk64();
         bwait(s_full + wg, s_ph, XF(4));
-        if (trw) IA_TRACE(4 + warp, 8, 2 * n_kt + n);
+        if (trw) IA_TRACE(4 + sw, 8, 2 * n_kt + n);
         s_ph ^= 1u;
         if (tm) IA_TADD(14, clk64() - tw0);
       }
@@ -673,7 +725,7 @@ __global__ void __launch_bounds__(Cfg<DP>::NTHREADS, 1)
       // the P.V that last read this P^ buffer must be done (first use passes at once)
       long long tq0 = clk64();
       mbar_wait(p_free + wg * C::NPB + pbl, ((uint32_t)(tl / C::NPB) & 1u) ^ 1u);
-      if (trw) IA_TRACE(4 + warp, 10, 2 * n_kt + n);
+      if (trw) IA_TRACE(4 + sw, 10, 2 * n_kt + n);
       if (tm) IA_TADD(13, clk64() - tq0);
 #pragma unroll 1
       for (int hb = 0; hb < BN / 64; ++hb) {
@@ -683,7 +735,7 @@ __global__ void __launch_bounds__(Cfg<DP>::NTHREADS, 1)
           tc_fence_before();
           __syncwarp();
           if (lane == 0) mbar_arrive(s_free + wg);
-          if (trw) IA_TRACE(4 + warp, 9, 2 * n_kt + n);
+          if (trw) IA_TRACE(4 + sw, 9, 2 * n_kt + n);
         }
         const int j0 = n * BN + hb * 64;
         uint32_t pk[16];
@@ -710,27 +762,37 @@ __global__ void __launch_bounds__(Cfg<DP>::NTHREADS, 1)
           }
         } else if (!p.mask_bits && fast && wtab) {
           const bool any_cut = __any_sync(0xffffffffu, cut < 64);
-          if (uncl3 && !any_cut) {
+          if (!any_cut && m9) {
+            // address = tab0 + ((umulhi(n, magic9) & ~511) | row*4): IMAD, IMAD.HI, LOP3,
+            // LDS per logit (+ the clip VIMNMX when the warp's index range exceeds the
+            // table).  Groups of 16 keys below every row's threshold stay zero.
+            const uint32_t nk2 = im.nk2, base = im.base;
+            const int32_t lo = im.lo;
+            auto groups = [&](auto clip) {
 #pragma unroll
-            for (int q = 0; q < 16; ++q) {
-              const uint32_t* v4 = q < 8 ? &va[4 * q] : &vb[4 * (q - 8)];
-              const uint32_t p0 = lds_u32(tab_row + (im.idx_u((int32_t)v4[0]) << 9));
-              const uint32_t p1 = lds_u32(tab_row + (im.idx_u((int32_t)v4[1]) << 9));
-              const uint32_t p2 = lds_u32(tab_row + (im.idx_u((int32_t)v4[2]) << 9));
-              const uint32_t p3 = lds_u32(tab_row + (im.idx_u((int32_t)v4[3]) << 9));
-              pk[q] = __byte_perm(__byte_perm(p0, p1, 0x0040), __byte_perm(p2, p3, 0x0040), 0x5410);
-            }
-          } else if (!any_cut && m9) {
-            // address = (umulhi(n, magic9) & ~511) | row*4: no shift, no address IMAD
+              for (int g = 0; g < 4; ++g) {
+                const uint32_t* v16 = g < 2 ? &va[16 * g] : &vb[16 * (g - 2)];
+                int32_t gm = (int32_t)v16[0];
 #pragma unroll
-            for (int q = 0; q < 16; ++q) {
-              const uint32_t* v4 = q < 8 ? &va[4 * q] : &vb[4 * (q - 8)];
-              const uint32_t p0 = lds_u32(tab0 + ((__umulhi(im.n_clip((int32_t)v4[0]), m9) & 0xFFFFFE00u) | row4));
-              const uint32_t p1 = lds_u32(tab0 + ((__umulhi(im.n_clip((int32_t)v4[1]), m9) & 0xFFFFFE00u) | row4));
-              const uint32_t p2 = lds_u32(tab0 + ((__umulhi(im.n_clip((int32_t)v4[2]), m9) & 0xFFFFFE00u) | row4));
-              const uint32_t p3 = lds_u32(tab0 + ((__umulhi(im.n_clip((int32_t)v4[3]), m9) & 0xFFFFFE00u) | row4));
-              pk[q] = __byte_perm(__byte_perm(p0, p1, 0x0040), __byte_perm(p2, p3, 0x0040), 0x5410);
-            }
+                for (int e = 1; e < 16; ++e) gm = max(gm, (int32_t)v16[e]);
+                if (!__any_sync(0xffffffffu, gm >= theta)) continue;  // pk stays 0
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                  const uint32_t* v4 = v16 + 4 * q;
+                  uint32_t pw[4];
+#pragma unroll
+                  for (int e = 0; e < 4; ++e) {
+                    const int32_t x = decltype(clip)::value ? max((int32_t)v4[e], lo) : (int32_t)v4[e];
+                    const uint32_t n = base + nk2 * (uint32_t)x;
+                    pw[e] = lds_u32(tab0 + and_or(__umulhi(n, m9), 0xFFFFFE00u, row4));
+                  }
+                  pk[4 * g + q] = __byte_perm(__byte_perm(pw[0], pw[1], 0x0040),
+                                              __byte_perm(pw[2], pw[3], 0x0040), 0x5410);
+                }
+              }
+            };
+            if (uncl3) groups(std::false_type{});
+            else groups(std::true_type{});
           } else if (!any_cut) {
 #pragma unroll
             for (int q = 0; q < 16; ++q) {
@@ -787,7 +849,7 @@ __global__ void __launch_bounds__(Cfg<DP>::NTHREADS, 1)
       fence_proxy_async_smem();
       __syncwarp();
       if (lane == 0) mbar_arrive(p_full + wg * C::NPB + pbl);
-      if (trw) IA_TRACE(4 + warp, 11, 2 * n_kt + n);
+      if (trw) IA_TRACE(4 + sw, 11, 2 * n_kt + n);
       ++tl;
     }
 
@@ -816,7 +878,7 @@ __global__ void __launch_bounds__(Cfg<DP>::NTHREADS, 1)
     named_bar_sync(1, NWT);
     const int rows = min(BM, p.L - q0);
     float* obase = p.out + ((size_t)bh * p.L + q0) * p.d;
-    const int tid = threadIdx.x;
+    const int tid = stid;
     if (p.d == DP) {  // compile-time row pitch: shifts instead of a division
       constexpr int D4 = DP / 4;
 #pragma unroll 1
@@ -847,7 +909,7 @@ __global__ void __launch_bounds__(Cfg<DP>::NTHREADS, 1)
   }
   tc_fence_before();
   __syncthreads();
-  if (threadIdx.x == 128 * NWG) { IA_TMARK(5); if (IA_PROFILE && p.dbg_times) p.dbg_times[(size_t)blockIdx.x * 16 + 10] = n_kt; }
+  if (rw == 0 && lane == 0) { IA_TMARK(5); if (IA_PROFILE && p.dbg_times) p.dbg_times[(size_t)blockIdx.x * 16 + 10] = n_kt; }
   if (rw == 2) {
     tc_fence_after();
     tmem_dealloc(tmem, TMEM_COLS);

@@ -24,6 +24,11 @@ __host__ __device__ inline int64_t compute_c_int(double c, int64_t d, float s_q,
   return ci < 1 ? 1 : ci;
 }
 
+// Entries of the fused kernel's per-row normalisation table: zero-extended to 56
+// for LUTs of <= 32 entries (rows whose largest reachable index is < 56 skip the
+// per-logit clip), else one per LUT entry.
+__host__ __device__ constexpr int row_table_entries(int nlut) { return nlut <= 32 ? 56 : nlut; }
+
 __host__ __device__ inline int bitlen_u64(uint64_t x) {
   int n = 0;
   while (x) { ++n; x >>= 1; }
@@ -85,13 +90,17 @@ __host__ __device__ inline void fill_head_params(int64_t c_int, int64_t dbound, 
     }
   }
   if (!hp->use32) hp->unc32 = 0;
-  // Scaled magic for the clipped range n <= (2k+1) c_eff: with M9 the magic of shift
-  // s9 <= 9 and magic9 = M9 << (9 - s9), umulhi(n, magic9) = idx * 512 + r with
-  // r < 512 (floor(floor(x * 2^j) / 2^j) = floor(x)), so a row-table address
-  // idx * 512 + row * 4 is one LOP3 away.  0 when it does not fit 32 bits.
+  // Scaled magic for every n whose index fits the fused kernel's zero-extended row
+  // table (idx <= NT9 = row_table_entries(nlut) - 1: n < 2 c_eff (NT9 + 1)), which
+  // covers the clipped range n <= (2k+1) c_eff and the unclipped n of any row whose
+  // largest reachable index fits the table: with M9 the magic of shift s9 <= 9 and
+  // magic9 = M9 << (9 - s9), umulhi(n, magic9) = idx * 512 + r with r < 512
+  // (floor(floor(x * 2^j) / 2^j) = floor(x)), so a row-table address idx * 512 +
+  // row * 4 is one LOP3 away.  0 when it does not fit 32 bits.
   hp->magic9 = 0;
   if (hp->use32) {
-    const int64_t nmc = (2 * k + 1) * c_eff;
+    const int64_t nt9 = row_table_entries(nlut) - 1;
+    const int64_t nmc = 2 * c_eff * (nt9 + 1) - 1;
     if (nmc < (int64_t(1) << 31)) {
       const uint64_t D = 2 * (uint64_t)c_eff;
       int s9 = bitlen_u64((uint64_t)nmc * D - 1) - 32;
@@ -155,6 +164,8 @@ struct IdxMap {
   __device__ __forceinline__ uint32_t n_clip(int32_t a) const {
     return base + nk2 * (uint32_t)max(a, lo);
   }
+  // n without the clip (unc32 rows whose largest index fits the table; operand of magic9)
+  __device__ __forceinline__ uint32_t n_unc(int32_t a) const { return base + nk2 * (uint32_t)a; }
   // Unclamped (hp.unc32): floor((2k*delta + c_eff) / (2 c_eff)) for any reachable
   // delta; may exceed k, callers index a table zero-extended past k.
   __device__ __forceinline__ uint32_t idx_u(int32_t a) const {

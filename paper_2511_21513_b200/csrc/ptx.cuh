@@ -60,15 +60,32 @@ __device__ __forceinline__ uint32_t mbar_try_wait(uint32_t bar, uint32_t parity)
 // of the CTA, so a spin count says nothing about elapsed time (a role that idles
 // through whole passes, or a kernel slowed down by a profiler's replay, would trip
 // a count-based limit).
+#ifndef IA_WAIT_STYLE
+#define IA_WAIT_STYLE 0
+#endif
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   const uint32_t a = smem_u32(bar);
   if (mbar_try_wait(a, parity)) return;
   const long long t0 = clock64();
+#if IA_WAIT_STYLE == 1
+  // retries unrolled 8x, the clock read once per 8 tries
+  for (;;) {
+#pragma unroll
+    for (int i = 0; i < 8; ++i)
+      if (mbar_try_wait(a, parity)) return;
+    if (clock64() - t0 > (1ll << 36)) __trap();
+  }
+#else
   uint32_t spins = 0;
   while (!mbar_try_wait(a, parity)) {
     if ((++spins & 1023u) == 0 && clock64() - t0 > (1ll << 36)) __trap();
   }
+#endif
 }
+
+// Wait with a fixed back-off between non-blocking tests instead of a suspended
+// try_wait (which wakes on every barrier event of the CTA).
+__device__ __forceinline__ void mbar_wait_backoff(uint64_t* bar, uint32_t parity, uint32_t ns);
 
 // Busy-poll variant for the single-thread producer / MMA-issuer roles, where the
 // ~220-cycle sleep wake-up would sit on the pipeline's critical path.
@@ -95,6 +112,14 @@ __device__ __forceinline__ uint32_t mbar_test(uint64_t* bar, uint32_t parity) {
       : "r"(smem_u32(bar)), "r"(parity)
       : "memory");
   return ok;
+}
+__device__ __forceinline__ void mbar_wait_backoff(uint64_t* bar, uint32_t parity, uint32_t ns) {
+  if (mbar_test(bar, parity)) return;
+  const long long t0 = clock64();
+  do {
+    __nanosleep(ns);
+    if (clock64() - t0 > (1ll << 36)) __trap();
+  } while (!mbar_test(bar, parity));
 }
 __device__ __forceinline__ void mbar_wait_spin(uint64_t* bar, uint32_t parity) {
   const uint32_t a = smem_u32(bar);

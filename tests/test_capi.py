@@ -114,6 +114,18 @@ def _check_map(hp, k, deltas):
         assert hp.use32 and int(n.max()) <= (2 * k + 1) * c_eff
         q9 = (n * np.uint64(hp.magic9)) >> np.uint64(32)
         assert np.array_equal(q9 & np.uint64(0xFFFFFE00), want * np.uint64(512))
+        # ... and for the UNCLIPPED n of rows whose largest index fits the kernel's
+        # zero-extended row table (idx <= NT9 = 55 for <= 32-entry LUTs)
+        nt9 = (56 if k + 1 <= 32 else k + 1) - 1
+        top = (2 * c_eff * (nt9 + 1) - 1 - c_eff) // (2 * k)  # largest delta with idx <= NT9
+        step = max(1, top // 2_000_000)
+        du = np.unique(np.concatenate([np.arange(0, top + 1, step, dtype=np.int64),
+                                       np.arange(max(0, top - 5000), top + 1, dtype=np.int64)]))
+        nu = (2 * k * du + c_eff).astype(np.uint64)
+        wu = nu // np.uint64(2 * c_eff)
+        assert int(wu.max()) <= nt9
+        qu = (nu * np.uint64(hp.magic9)) >> np.uint64(32)
+        assert np.array_equal(qu & np.uint64(0xFFFFFE00), wu * np.uint64(512))
 
 
 @pytest.mark.parametrize("b", [2, 5, 8])
