@@ -19,7 +19,8 @@
 extern "C" {
 #endif
 
-#define IA_ABI_VERSION 3  /* 2: ia_head_params gained magic9; 3: ia_attn_args.softmax_mode */
+#define IA_ABI_VERSION 4  /* 2: ia_head_params gained magic9; 3: ia_attn_args.softmax_mode;
+                            4: grouped-K fields of ia_attn_args, ia_group_params */
 #define IA_MAX_SEQ_LEN 65536   /* gemm.py:26 MAX_SEQ_LEN */
 #define IA_MAX_HEAD_DIM 131070 /* gemm.py:25 MAX_HEAD_DIM */
 #define IA_FUSED_MAX_HEAD_DIM 256
@@ -125,6 +126,21 @@ typedef struct ia_head_params {
 
 int ia_head_params_host(double c, int64_t d, int nlut, int p_scale, float s_q, float s_k,
                         float s_v, ia_head_params* out);
+/* Index map of one (query head, key group) of the grouped-K fused kernel: c_eff and
+ * the magic numbers of ia_head_params for c_int = round(c / alpha_g), alpha_g =
+ * f64(s_q) f64(s_k[g]) / sqrt(d) (softmax.py:370-378).  A group whose c_eff does
+ * not fit 31 bits has idx = 0 for every reachable delta and is stored as magic 0. */
+typedef struct ia_group_params {
+  int32_t c_eff;
+  uint32_t magic;
+  int32_t shift;
+  int32_t use32;
+} ia_group_params;
+/* out[(b*H + h) * n_groups + g] from q_scales [B*H] and k_scales [B*Hkv, n_groups]
+ * (device arrays, stream-ordered). */
+int ia_group_params_dev(const float* q_scales, const float* k_scales, int64_t B, int64_t H,
+                        int64_t Hkv, int64_t n_groups, int64_t d, double c, int nlut,
+                        ia_group_params* out, void* stream);
 /* Index-map parameters for a given c_int (clamped to 2^52 as softmax.py:277)
  * and an upper bound on delta = rowmax - logit (2^32 - 1 covers any int32
  * logits); used with ia_index_softmax. */
@@ -165,6 +181,12 @@ typedef struct ia_attn_args {
                            IA_SOFTMAX_FLOAT: the quant-only comparator's dequantise -> f32
                            softmax -> requantise path (pipeline.py:259-296), with MUFU exp2,
                            so P^ matches the reference to float tolerance, not bit for bit */
+  /* Grouped K (per-row-group key scales; softmax.py:309-399 default mode, pipeline.py:
+   * 229-246): k_group_size keys (a power of two in [8, 128]) share one K scale, and
+   * kgroup_params [B*H, ceil(L / k_group_size)] (device, from ia_group_params_dev)
+   * holds each (query head, key group)'s index map.  k_group_size = 0: per-head K. */
+  const struct ia_group_params* kgroup_params;
+  int32_t k_group_size;
 } ia_attn_args;
 #define IA_SOFTMAX_INDEX 0
 #define IA_SOFTMAX_FLOAT 1

@@ -13,6 +13,7 @@ because the reference builds its table with numpy's f64 ``exp``
 from __future__ import annotations
 
 import ctypes
+import math
 import os
 import subprocess
 
@@ -255,3 +256,36 @@ def quant_only_attention(q, k, v, mask=None, p_scale=P_UINT8X255):
     acc = phat.astype(np.int64) @ vq.astype(np.int64)
     out = acc.astype(np.float32) * np.float32(float(sv) / p_scale)
     return out, phat
+
+
+def attention_grouped_batched(q, k, v, k_group_size, *, causal=False, mask=None, b=5, c=6.6,
+                              p_scale=P_UINT8X255):
+    """Grouped-K pipeline (pipeline.py:229-246) per (b, head) unit, batched: Q and V
+    quantised per (b, head), K per (b, KV head, group of k_group_size keys)
+    (quantize.py:104-123 with per_row_group), int32 logits, the grouped IndexSoftmax
+    (softmax.py:309-399, default per-group max) and the exact P.V + rescale
+    (pipeline.py:248-252).  Plain composition of the oracle's stage functions."""
+    q = np.ascontiguousarray(q, np.float32)
+    B, H, L, d = q.shape
+    Hkv = k.shape[1]
+    g = H // Hkv
+    G = L // k_group_size
+    lut = build_lut(b, c)
+    m = None
+    if causal:
+        m = np.triu(np.ones((L, L), bool), 1)
+    if mask is not None:
+        m = np.asarray(mask, bool) if m is None else (m | np.asarray(mask, bool))
+    groups = (np.arange(L) // k_group_size).astype(np.int64)
+    out = np.zeros(q.shape, np.float32)
+    for bb in range(B):
+        for h in range(H):
+            qh, sq = quantize_tensor(q[bb, h])
+            kh, sk = quantize_groups(k[bb, h // g], G)
+            vh, sv = quantize_tensor(v[bb, h // g])
+            logits = matmul_s8(qh, kh)
+            cis = [c_int_from_alpha(c, float(sq) * float(s) / math.sqrt(d)) for s in sk]
+            prob = index_softmax_grouped(logits, groups, cis, lut, m, p_scale)
+            acc = gemm_pv(prob, vh)
+            out[bb, h] = acc.astype(np.float32) * np.float32(float(sv) / p_scale)
+    return out

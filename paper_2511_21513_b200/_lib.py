@@ -33,7 +33,7 @@ EXPORTS = (
     "ia_quant_amax_rows", "ia_quant_amax_cols", "ia_quant_scales", "ia_quantize",
     "ia_dequantize", "ia_quant_heads", "ia_quant_tensors", "ia_head_params_host", "ia_softmax_params_host", "ia_head_params_dev",
     "ia_mask_pack", "ia_attn_fwd", "ia_attn_supported", "ia_index_softmax", "ia_index_softmax_grouped",
-    "ia_gemm_i8", "ia_copy_rows_async",
+    "ia_gemm_i8", "ia_copy_rows_async", "ia_group_params_dev",
 )
 
 
@@ -55,7 +55,10 @@ class AttnArgs(ctypes.Structure):
                 ("nlut", ctypes.c_int32), ("p_scale", ctypes.c_int32),
                 ("lut", ctypes.c_uint8 * 256), ("dbg_logits", ctypes.c_void_p),
                 ("dbg_prob", ctypes.c_void_p), ("dbg_acc", ctypes.c_void_p),
-                ("dbg_times", ctypes.c_void_p), ("softmax_mode", ctypes.c_int32)]
+                ("dbg_times", ctypes.c_void_p), ("softmax_mode", ctypes.c_int32),
+                ("kgroup_params", ctypes.c_void_p), ("k_group_size", ctypes.c_int32)]
+
+GROUP_PARAMS_BYTES = 16  # ia_group_params {c_eff, magic, shift, use32}
 
 IA_SOFTMAX_INDEX = 0
 IA_SOFTMAX_FLOAT = 1
@@ -114,6 +117,8 @@ def load():
             "ia_index_softmax_grouped": ([P, i64, i64, P, i32, P, P, i32, i32, P, P, P], i32),
             "ia_gemm_i8": ([P, i64, i32, P, i64, i64, i64, i64, P, i64, P], i32),
             "ia_copy_rows_async": ([P, i64, P, i64, i64, i64, P], i32),
+            "ia_group_params_dev": ([P, P, i64, i64, i64, i64, i64, ctypes.c_double, i32, P, P],
+                                    i32),
         }
         for name, (args, res) in sig.items():
             fn = getattr(L, name)

@@ -24,7 +24,7 @@ from .pipeline import AttentionConfig
 
 def int_attention_batched(q, k, v, *, causal=False, seq_lens=None, mask=None,
                           scale_granularity="head", cfg=None, out=None, debug=False,
-                          check_finite=True, softmax="index"):
+                          check_finite=True, softmax="index", k_group_size=None):
     """Fused IntAttention over all (b, h) units.
 
     q: [B, H, L, d] f32; k, v: [B, Hkv, L, d] f32 with H % Hkv == 0.
@@ -34,6 +34,9 @@ def int_attention_batched(q, k, v, *, causal=False, seq_lens=None, mask=None,
     scale_granularity: "head" (one scale per (b, head) slab over its valid rows)
     or "tensor" (one global scale per Q/K/V tensor).
     cfg: AttentionConfig for b, c and p_format (granularity/mask/threads unused).
+    k_group_size: grouped K -- one K scale per (b, KV head, group of k_group_size keys)
+    and the grouped IndexSoftmax (softmax.py:309-399; a power of two in [8, 128]
+    dividing L, d <= 128), fused in one launch.
     Returns out [B, H, L, d] f32 (numpy in -> numpy out), plus a dict of stage
     tensors (quantised operands, int32 logits, u8 P, int32 acc) with debug=True.
     """
@@ -53,7 +56,8 @@ def int_attention_batched(q, k, v, *, causal=False, seq_lens=None, mask=None,
         raise ValueError("empty attention problem")
     numpy_in = not is_torch(q)
     host_in = all((not is_torch(x)) or x.device.type == "cpu" for x in (q, k, v))
-    if host_in and not debug and scale_granularity == "head" and B * ks[1] > 1 and softmax == "index":
+    if (host_in and not debug and scale_granularity == "head" and B * ks[1] > 1
+            and softmax == "index" and k_group_size is None):
         return _host_pipelined(q, k, v, causal=causal, seq_lens=seq_lens, mask=mask, cfg=cfg,
                                out=out, check_finite=check_finite, numpy_in=numpy_in)
     qt, kt, vt = (to_device(x, np.float32) for x in (q, k, v))
@@ -79,7 +83,7 @@ def int_attention_batched(q, k, v, *, causal=False, seq_lens=None, mask=None,
     res = E.attention(qt, kt, vt, causal=causal, seq_lens=sl, mask=mt,
                       scale_granularity=scale_granularity, b=cfg.b, c=cfg.c,
                       p_scale=cfg.p_format.value, out=o, debug=debug,
-                      check_finite=check_finite, softmax=softmax)
+                      check_finite=check_finite, softmax=softmax, k_group_size=k_group_size)
     dbg = None
     if debug:
         res, dbg = res

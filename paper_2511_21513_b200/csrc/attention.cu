@@ -59,6 +59,9 @@ struct AttnDev {
   // 1 pass 1 only; 2/4/8/16 spin instead of sleep-waits (QK^T issuer / softmax s_full /
   // P.V issuer / TMA producers); 32 no pass-1 arithmetic; 256 generic index map (no magic9)
   int xflags;
+  // grouped K (per-row-group key scales): per (b*H + h, group) {c_eff, magic, shift, use32}
+  const int4* kgroup;
+  int gs_log2, n_groups;
   uint8_t lut[256];
 };
 
@@ -205,7 +208,244 @@ __device__ __forceinline__ void iwait(uint64_t* bar, uint32_t parity, bool spin)
   else bwait(bar, parity, spin);
 }
 
-template <int DP, bool DEBUG, bool SKEL = false, bool QO = false>
+// ------------------------------------------------------------------ grouped K
+// Grouped-K IndexSoftmax (softmax.py:309-399, default per-group-max mode, as the
+// per-row-group-K pipeline uses it, pipeline.py:229-246).  Keys are quantised per
+// row group of gs keys, so group g has its own clip threshold c_g (from alpha_g =
+// s_q s_k[g] / sqrt(d)) and every distance is taken against the group's own row
+// max m_g; the LUT and the integer row normalisation are shared.  For gs | 128 no
+// group straddles a key tile, so a tile's group maxima come from the tile itself
+// and the fused kernel needs two passes instead of three: pass A (S = sum e) and
+// pass B (P^ -> P.V), each reading its tile from TMEM twice -- group maxima over
+// 8-key chunks, then the per-logit work.  The int32 logits still never leave the SM.
+
+// Excluded-key bits (bit e = key j0 + e masked) for 32 keys of row i.
+__device__ __forceinline__ uint32_t gk_mask32(const AttnDev& p, bool row_valid, int i, int j0,
+                                              int lim) {
+  return row_valid ? chunk_mask(p, i, j0, lim) : 0xffffffffu;
+}
+
+// Group maxima of one 128-key tile: gm[c] = max over the unmasked keys of the group
+// holding 8-key chunk c (INT_MIN if the row has none there).
+__device__ __forceinline__ void gk_group_max(const AttnDev& p, uint32_t s_tile, bool row_valid,
+                                             int i, int j0t, int lim, int32_t (&gm)[16]) {
+#pragma unroll
+  for (int hb = 0; hb < 2; ++hb) {
+    uint32_t va[32], vb[32];
+    tmem_ld64(s_tile + hb * 64, va, vb);
+    const int j0 = j0t + hb * 64;
+    const uint32_t ma = gk_mask32(p, row_valid, i, j0, lim);
+    const uint32_t mb = gk_mask32(p, row_valid, i, j0 + 32, lim);
+#pragma unroll
+    for (int c = 0; c < 8; ++c) {
+      const uint32_t* v8 = c < 4 ? &va[8 * c] : &vb[8 * (c - 4)];
+      const uint32_t bits = ((c < 4 ? ma : mb) >> (8 * (c & 3))) & 0xffu;
+      int32_t x = INT_MIN;
+#pragma unroll
+      for (int e = 0; e < 8; ++e)
+        if (!((bits >> e) & 1u)) x = max(x, (int32_t)v8[e]);
+      gm[hb * 8 + c] = x;
+    }
+  }
+  // chunks of one group share its maximum (groups of gs/8 = 1..16 chunks)
+  const int gs8 = 1 << (p.gs_log2 - 3);
+#pragma unroll
+  for (int s = 1; s < 16; s <<= 1) {
+    if (gs8 > s) {
+#pragma unroll
+      for (int c = 0; c < 16; ++c)
+        if (!(c & s)) {
+          const int32_t t = max(gm[c], gm[c | s]);
+          gm[c] = t;
+          gm[c | s] = t;
+        }
+    }
+  }
+}
+
+// idx of logit a in a group with row max m (softmax.py:380-386 with the group's c).
+struct GkMap {
+  int32_t lo;
+  uint32_t base, magic, shift;
+  int64_t c_eff;
+  int32_t m;
+  bool use32;
+  __device__ __forceinline__ void init(int32_t gmax, int4 g, uint32_t k) {
+    c_eff = (int64_t)g.x;
+    magic = (uint32_t)g.y;
+    shift = (uint32_t)g.z;
+    use32 = g.w != 0;
+    m = gmax;
+    lo = idx_lo(gmax, c_eff);
+    base = (uint32_t)gmax * (2u * k) + (uint32_t)c_eff;
+  }
+  __device__ __forceinline__ uint32_t idx32(int32_t a, uint32_t nk2) const {
+    const uint32_t n = base + nk2 * (uint32_t)max(a, lo);
+    return __umulhi(n, magic) >> shift;
+  }
+  __device__ __forceinline__ uint32_t idx(int32_t a, uint32_t nk2, uint32_t k) const {
+    return use32 ? idx32(a, nk2) : idx_slow(m, a, c_eff, k);
+  }
+};
+
+template <int DP, bool DEBUG>
+__device__ __forceinline__ void gk_passes(const AttnDev& p, uint8_t* smem, uint32_t* tab,
+                                          uint32_t* xsum, const uint8_t* lut8, uint64_t* s_full,
+                                          uint64_t* s_free, uint64_t* p_full, uint64_t* p_free,
+                                          uint32_t s_base, int wg, int row, int lane, int i,
+                                          int lim, int bh, int n_kt, bool row_valid,
+                                          bool resident, uint32_t& s_ph) {
+  using C = Cfg<DP>;
+  constexpr int NWG = C::NWG;
+  constexpr int NWT = 128 * NWG;
+  const int nlut = p.nlut;
+  const uint32_t k = (uint32_t)(nlut - 1);
+  uint32_t nk2 = 0u - 2u * k;
+  asm("" : "+r"(nk2));
+  const int4* gp = p.kgroup + (size_t)bh * p.n_groups;
+
+  // ---- pass A: e = lut[idx_g], S = sum e (softmax.py:380-394); the only wait on the
+  // MMA when the logits stay resident in TMEM
+  uint32_t S = 0;
+  for (int n = wg; n < n_kt; n += NWG) {
+    mbar_wait(s_full + wg, s_ph);
+    s_ph ^= 1u;
+    tc_fence_after();
+    int32_t gm[16];
+    gk_group_max(p, s_base, row_valid, i, n * BN, lim, gm);
+#pragma unroll 1
+    for (int hb = 0; hb < 2; ++hb) {
+      uint32_t va[32], vb[32];
+      tmem_ld64(s_base + hb * 64, va, vb);
+      if (hb == 1 && !resident) {
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(s_free + wg);
+      }
+      const int j0 = n * BN + hb * 64;
+      const uint32_t ma = gk_mask32(p, row_valid, i, j0, lim);
+      const uint32_t mb = gk_mask32(p, row_valid, i, j0 + 32, lim);
+      const bool open = !__any_sync(0xffffffffu, (ma | mb) != 0u);  // no key masked in the warp
+#pragma unroll
+      for (int c = 0; c < 8; ++c) {
+        const int32_t gmax = hb ? gm[8 + c] : gm[c];
+        if (gmax == INT_MIN) continue;  // every key of the chunk is masked: e = 0
+        GkMap gmap;
+        gmap.init(gmax, __ldg(gp + ((j0 + 8 * c) >> p.gs_log2)), k);
+        const uint32_t* v8 = c < 4 ? &va[8 * c] : &vb[8 * (c - 4)];
+        const uint32_t bits = ((c < 4 ? ma : mb) >> (8 * (c & 3))) & 0xffu;
+        if (open && gmap.use32) {  // warp-uniform: the common case, no per-key tests
+#pragma unroll
+          for (int e = 0; e < 8; ++e) S += lut8[gmap.idx32((int32_t)v8[e], nk2)];
+        } else {
+#pragma unroll
+          for (int e = 0; e < 8; ++e)
+            if (!((bits >> e) & 1u)) S += lut8[gmap.idx((int32_t)v8[e], nk2, k)];
+        }
+      }
+    }
+  }
+  // ---- shared row normalisation table (softmax.py:300-306): (2 scale lut[t] + S) // 2S
+  xsum[wg * 128 + row] = S;
+  named_bar_sync(1, NWT);
+  S = xsum[row];
+#pragma unroll
+  for (int w = 1; w < NWG; ++w) S += xsum[w * 128 + row];
+  {
+    const uint32_t two_s = 2u * S;
+    const float rden = S ? __frcp_rn((float)two_s) : 0.0f;
+    for (int t = wg; t < nlut; t += NWG) {
+      const uint32_t lt = lut8[t];
+      uint32_t pv = 0u;
+      if (S && lt) {
+        const uint32_t num = (uint32_t)p.scale_x2 * lt + S;
+        int32_t q = __float2int_rz(__fmul_rn((float)num, rden));
+        const int32_t r = (int32_t)num - q * (int32_t)two_s;
+        q += r < 0 ? -1 : (r >= (int32_t)two_s ? 1 : 0);
+        pv = (uint32_t)q;
+      }
+      tab[t * 128 + row] = pv;
+    }
+  }
+  named_bar_sync(1, NWT);
+
+  // ---- pass B: P^ = rowtab[idx_g] -> smem -> P.V MMA
+  const uint32_t tab_row = smem_u32(tab) + (uint32_t)row * 4u;
+  const uint32_t p_rows = smem_u32(smem + C::OFF_P + wg * C::NPB * C::P_BYTES) + (uint32_t)row * 128;
+  const uint32_t p_xor = (uint32_t)(row & 7);
+  int tl = 0;
+  for (int n = wg; n < n_kt; n += NWG) {
+    if (!resident) {
+      mbar_wait(s_full + wg, s_ph);
+      s_ph ^= 1u;
+    }
+    tc_fence_after();
+    const int pbl = tl % C::NPB;
+    const uint32_t p_row = p_rows + (uint32_t)(pbl * C::P_BYTES);
+    mbar_wait(p_free + wg * C::NPB + pbl, ((uint32_t)(tl / C::NPB) & 1u) ^ 1u);
+    int32_t gm[16];
+    gk_group_max(p, s_base, row_valid, i, n * BN, lim, gm);
+#pragma unroll 1
+    for (int hb = 0; hb < 2; ++hb) {
+      uint32_t va[32], vb[32];
+      tmem_ld64(s_base + hb * 64, va, vb);
+      if (hb == 1 && !resident) {
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(s_free + wg);
+      }
+      const int j0 = n * BN + hb * 64;
+      const uint32_t ma = gk_mask32(p, row_valid, i, j0, lim);
+      const uint32_t mb = gk_mask32(p, row_valid, i, j0 + 32, lim);
+      uint32_t pk[16];
+#pragma unroll
+      for (int q = 0; q < 16; ++q) pk[q] = 0u;
+      const bool open = !__any_sync(0xffffffffu, (ma | mb) != 0u);
+#pragma unroll
+      for (int c = 0; c < 8; ++c) {
+        const int32_t gmax = hb ? gm[8 + c] : gm[c];
+        if (gmax == INT_MIN) continue;
+        GkMap gmap;
+        gmap.init(gmax, __ldg(gp + ((j0 + 8 * c) >> p.gs_log2)), k);
+        const uint32_t* v8 = c < 4 ? &va[8 * c] : &vb[8 * (c - 4)];
+        const uint32_t bits = ((c < 4 ? ma : mb) >> (8 * (c & 3))) & 0xffu;
+        if (open && gmap.use32) {
+#pragma unroll
+          for (int q = 0; q < 2; ++q) {
+            const uint32_t p0 = lds_u32(tab_row + (gmap.idx32((int32_t)v8[4 * q], nk2) << 9));
+            const uint32_t p1 = lds_u32(tab_row + (gmap.idx32((int32_t)v8[4 * q + 1], nk2) << 9));
+            const uint32_t p2 = lds_u32(tab_row + (gmap.idx32((int32_t)v8[4 * q + 2], nk2) << 9));
+            const uint32_t p3 = lds_u32(tab_row + (gmap.idx32((int32_t)v8[4 * q + 3], nk2) << 9));
+            pk[2 * c + q] = __byte_perm(__byte_perm(p0, p1, 0x0040), __byte_perm(p2, p3, 0x0040), 0x5410);
+          }
+        } else {
+#pragma unroll
+          for (int e = 0; e < 8; ++e)
+            if (!((bits >> e) & 1u))
+              pk[2 * c + (e >> 2)] |= lds_u32(tab_row + (gmap.idx((int32_t)v8[e], nk2, k) << 9))
+                                      << (8 * (e & 3));
+        }
+      }
+      if (DEBUG && p.dbg_prob && i < p.L) {
+#pragma unroll
+        for (int e = 0; e < 64; ++e)
+          if (j0 + e < p.L)
+            p.dbg_prob[((size_t)bh * p.L + i) * p.L + j0 + e] = (uint8_t)(pk[e >> 2] >> (8 * (e & 3)));
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const uint32_t x = (uint32_t)(4 * hb + u);
+        sts128(p_row + ((x ^ p_xor) << 4), pk[4 * u], pk[4 * u + 1], pk[4 * u + 2], pk[4 * u + 3]);
+      }
+    }
+    fence_proxy_async_smem();
+    __syncwarp();
+    if (lane == 0) mbar_arrive(p_full + wg * C::NPB + pbl);
+    ++tl;
+  }
+}
+
+template <int DP, bool DEBUG, bool SKEL = false, bool QO = false, bool GK = false>
 __global__ void __launch_bounds__(Cfg<DP>::NTHREADS, 1)
     attn_fwd_kernel(const __grid_constant__ CUtensorMap tmq,
                     const __grid_constant__ CUtensorMap tmk,
@@ -265,8 +505,9 @@ __global__ void __launch_bounds__(Cfg<DP>::NTHREADS, 1)
   const bool resident = n_kt <= NWG;  // every logit tile fits its own TMEM buffer
   // QO (quant-only comparator, pipeline.py:259-296): an online f32 max / sum-of-exp
   // pass, then the P / P.V pass -- two passes instead of IndexSoftmax's three.
-  const int npass = resident ? 1 : ((XF(1)) ? 1 : (QO ? 2 : 3));
-  constexpr int PV_PASS = QO ? 1 : 2;  // tile t >= PV_PASS * n_kt belongs to the P / P.V pass
+  // GK (grouped K): pass A (S) + pass B (P / P.V), group maxima taken per tile.
+  const int npass = resident ? 1 : (XF(1) ? 1 : ((QO || GK) ? 2 : 3));
+  constexpr int PV_PASS = (QO || GK) ? 1 : 2;  // tile t >= PV_PASS * n_kt: the P / P.V pass
   const int n_kt_b = (XF(1)) ? 0 : n_kt;  // key tiles of passes 2-3 / P.V
 
   if (rw == 0 && lane == 0) {
@@ -453,6 +694,11 @@ __global__ void __launch_bounds__(Cfg<DP>::NTHREADS, 1)
     const bool tm = (stid == 0);
     const bool trw = IA_PROFILE && lane == 0;  // one trace segment per softmax warp
     if (tm) IA_TMARK(0);
+    if constexpr (GK) {
+      gk_passes<DP, DEBUG>(p, smem, reinterpret_cast<uint32_t*>(tab), xsum, lut8, s_full, s_free,
+                           p_full, p_free, s_base, wg, row, lane, i, lim, bh, n_kt, row_valid,
+                           resident, s_ph);
+    } else {
     // ---- pass 1: row max over unmasked keys (softmax.py:139-143, :174-179); the row
     // min rides along (free: pass 1 waits on the MMA) to size the unclipped index range
     int32_t mx = INT_MIN, mn = INT_MAX;
@@ -852,6 +1098,7 @@ __global__ void __launch_bounds__(Cfg<DP>::NTHREADS, 1)
       if (trw) IA_TRACE(4 + sw, 11, 2 * n_kt + n);
       ++tl;
     }
+    }  // !GK
 
     // ---- epilogue: out = f32(acc) * f32(s_v / scale) (pipeline.py:250-252)
     // TMEM -> registers -> smem staging (all TMA/MMA traffic has drained once
@@ -925,7 +1172,7 @@ bool attn_supported(int nlut) {
   return attn_smem_bytes<DP>(nlut) + 256 <= 227 * 1024;
 }
 
-template <int DP, bool DEBUG, bool SKEL = false, bool QO = false>
+template <int DP, bool DEBUG, bool SKEL = false, bool QO = false, bool GK = false>
 static int launch_attn(const ia_attn_args* a, cudaStream_t st) {
   using C = Cfg<DP>;
   if (!attn_supported<DP>(a->nlut))
@@ -964,10 +1211,19 @@ static int launch_attn(const ia_attn_args* a, cudaStream_t st) {
   dv.n_qt = (int)((a->L + BM - 1) / BM);
   static const int xflags = dev_knob("IA_XFLAGS", 0);  // always 0 in the release build
   dv.xflags = xflags;
+  dv.kgroup = reinterpret_cast<const int4*>(a->kgroup_params);
+  dv.gs_log2 = 0;
+  dv.n_groups = 0;
+  if (GK) {
+    int lg = 0;
+    while ((1 << lg) < a->k_group_size) ++lg;
+    dv.gs_log2 = lg;
+    dv.n_groups = (int)((a->L + a->k_group_size - 1) / a->k_group_size);
+  }
   for (int t = 0; t < 256; ++t) dv.lut[t] = t < a->nlut ? a->lut[t] : 0;
   size_t smem = attn_smem_bytes<DP>(a->nlut);
   if (smem < 120 * 1024) smem = 120 * 1024;  // one CTA per SM (it owns all 512 TMEM columns)
-  auto kern = attn_fwd_kernel<DP, DEBUG, SKEL, QO>;
+  auto kern = attn_fwd_kernel<DP, DEBUG, SKEL, QO, GK>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return fail(IA_ERR_CUDA, "smem attribute: %s", cudaGetErrorString(e));
   const uint64_t grid = (uint64_t)dv.n_qt * BH;
@@ -1011,6 +1267,8 @@ extern "C" int ia_attn_fwd(const ia_attn_args* a, void* stream) {
     return fail(IA_ERR_INVALID_ARGUMENT, "operands must be 16-byte aligned");
   cudaStream_t st = (cudaStream_t)stream;
   const bool dbg = a->dbg_logits || a->dbg_prob || a->dbg_acc;
+  if (a->k_group_size && a->softmax_mode != IA_SOFTMAX_INDEX)
+    return fail(IA_ERR_INVALID_ARGUMENT, "grouped K is an IndexSoftmax mode");
   if (a->softmax_mode == IA_SOFTMAX_FLOAT) {  // quant-only comparator
     switch (a->d_pad) {
       case 32: return dbg ? launch_attn<32, true, false, true>(a, st) : launch_attn<32, false, false, true>(a, st);
@@ -1021,6 +1279,20 @@ extern "C" int ia_attn_fwd(const ia_attn_args* a, void* stream) {
   }
   if (a->softmax_mode != IA_SOFTMAX_INDEX)
     return fail(IA_ERR_INVALID_ARGUMENT, "ia_attn_fwd: unknown softmax_mode %d", a->softmax_mode);
+  if (a->k_group_size) {  // grouped K (softmax.py:309-399)
+    const int gs = a->k_group_size;
+    if (gs < 8 || gs > 128 || (gs & (gs - 1)) || !a->kgroup_params)
+      return fail(IA_ERR_INVALID_ARGUMENT,
+                  "grouped K needs k_group_size a power of two in [8, 128] and kgroup_params");
+    if (a->nlut > 64)
+      return fail(IA_ERR_INVALID_ARGUMENT, "grouped K supports LUTs of <= 64 entries");
+    switch (a->d_pad) {
+      case 32: return dbg ? launch_attn<32, true, false, false, true>(a, st) : launch_attn<32, false, false, false, true>(a, st);
+      case 64: return dbg ? launch_attn<64, true, false, false, true>(a, st) : launch_attn<64, false, false, false, true>(a, st);
+      case 128: return dbg ? launch_attn<128, true, false, false, true>(a, st) : launch_attn<128, false, false, false, true>(a, st);
+      default: return fail(IA_ERR_HEAD_DIM, "grouped K: fused path supports d <= 128");
+    }
+  }
   switch (a->d_pad) {
     case 32: return dbg ? launch_attn<32, true>(a, st) : launch_attn<32, false>(a, st);
     case 64: return dbg ? launch_attn<64, true>(a, st) : launch_attn<64, false>(a, st);

@@ -68,6 +68,31 @@ __global__ void head_params_kernel(const float* __restrict__ qs, const float* __
   out[u] = hp;
 }
 
+__global__ void group_params_kernel(const float* __restrict__ qs, const float* __restrict__ ks,
+                                    int64_t B, int64_t H, int64_t Hkv, int64_t G, int64_t d,
+                                    double c, int nlut, ia_group_params* __restrict__ out) {
+  const int64_t u = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (u >= B * H * G) return;
+  const int64_t bh = u / G, g = u - bh * G;
+  const int64_t b = bh / H, h = bh - b * H;
+  const int64_t ku = b * Hkv + h / (H / Hkv);
+  ia_head_params hp;
+  fill_head_params(compute_c_int(c, d, qs[bh], ks[ku * G + g]), 2 * d * 127 * 127, nlut, &hp);
+  ia_group_params gp;
+  if (hp.c_eff > INT32_MAX) {  // c_int > 2k * dbound: idx = 0 for every reachable delta
+    gp.c_eff = INT32_MAX;
+    gp.magic = 0u;
+    gp.shift = 0;
+    gp.use32 = 1;
+  } else {
+    gp.c_eff = (int32_t)hp.c_eff;
+    gp.magic = hp.magic;
+    gp.shift = hp.shift;
+    gp.use32 = hp.use32;
+  }
+  out[u] = gp;
+}
+
 __global__ void mask_pack_kernel(const uint8_t* __restrict__ mask, int64_t L, int64_t W,
                                  uint32_t* __restrict__ bits) {
   const int64_t n = L * W;
@@ -149,6 +174,18 @@ extern "C" int ia_head_params_dev(const float* q_scales, const float* k_scales,
       q_scales, k_scales, v_scales, q_per_head, kv_per_head, B, H, Hkv, d, c, nlut, p_scale,
       out);
   return check_launch("head_params_kernel");
+}
+
+extern "C" int ia_group_params_dev(const float* q_scales, const float* k_scales, int64_t B,
+                                   int64_t H, int64_t Hkv, int64_t n_groups, int64_t d, double c,
+                                   int nlut, ia_group_params* out, void* stream) {
+  if (!q_scales || !k_scales || !out || B < 1 || H < 1 || Hkv < 1 || H % Hkv || n_groups < 1 ||
+      d < 1 || nlut < 4 || nlut > 256)
+    return fail(IA_ERR_INVALID_ARGUMENT, "ia_group_params_dev: bad arguments");
+  const int64_t n = B * H * n_groups;
+  group_params_kernel<<<(unsigned)((n + 127) / 128), 128, 0, (cudaStream_t)stream>>>(
+      q_scales, k_scales, B, H, Hkv, n_groups, d, c, nlut, out);
+  return check_launch("group_params_kernel");
 }
 
 extern "C" int ia_mask_pack(const uint8_t* mask, int64_t L, uint32_t* bits, void* stream) {

@@ -229,6 +229,53 @@ def prepare(q, k, v, *, seq_lens=None, scale_granularity="head", b=5, c=6.6, p_s
                            d_pad, l_pad)
 
 
+def prepare_grouped(q, k, v, k_group_size, *, b=5, c=6.6, p_scale=255, d_pad=None):
+    """Grouped-K quantisation (pipeline.py:217-219 with a per_row_group K granularity,
+    quantize.py:92-123): Q and V one scale per (b, head), K one scale per (b, KV head,
+    group of ``k_group_size`` keys); plus the per-(query head, key group) index maps
+    (ia_group_params_dev) the grouped fused kernel reads.  Returns (Prepared, gparams)."""
+    B, H, Lq, d = q.shape
+    Hkv = k.shape[1]
+    dev = q.device
+    gs = int(k_group_size)
+    G = Lq // gs
+    if d_pad is None:
+        d_pad = pad_head_dim(d)
+    l_pad = _round_up(Lq, 16)
+    ws = Workspace(B * H + B * Hkv * G + B * Hkv, dev)
+    aq, sq = ws.take(B * H)
+    ak, sk = ws.take(B * Hkv * G)
+    av, sv = ws.take(B * Hkv)
+    amax_rows(q, B * H, Lq, d, aq, ws.err)
+    amax_rows(k, B * Hkv * G, gs, d, ak, ws.err)
+    amax_rows(v, B * Hkv, Lq, d, av, ws.err)
+    scales_from_amax(ws.amax, ws.scales)
+    qhat = torch.empty((B * H, Lq, d_pad), dtype=torch.int8, device=dev)
+    khat = torch.empty((B * Hkv, Lq, d_pad), dtype=torch.int8, device=dev)
+    vt = torch.empty((B * Hkv, d_pad, l_pad), dtype=torch.int8, device=dev)
+    quantize_rows(q, B * H, Lq, d, sq, qhat, d_pad)
+    quantize_rows(k, B * Hkv * G, gs, d, sk, khat, d_pad)
+    quantize_vt(v, B * Hkv, Lq, d, sv, vt, l_pad, d_pad * l_pad)
+    # per-(b, h) parameters: only out_scale = s_v / p_scale is read in grouped mode (the
+    # K-side index maps are per group, below); sv stands in for the per-head K scale
+    params = torch.empty((B * H, HEAD_PARAMS_BYTES), dtype=torch.uint8, device=dev)
+    _lib.check(_lib.load().ia_head_params_dev(_p(sq), _p(sv), _p(sv), 1, 1, B, H, Hkv, d,
+                                              float(c), 1 << b, int(p_scale), _p(params),
+                                              _stream()), "head params")
+    gparams = torch.empty((B * H, G, _lib.GROUP_PARAMS_BYTES), dtype=torch.uint8, device=dev)
+    _lib.check(_lib.load().ia_group_params_dev(_p(sq), _p(sk), B, H, Hkv, G, d, float(c),
+                                               1 << b, _p(gparams), _stream()), "group params")
+    return Prepared(qhat, khat, vt, sq, sk, sv, params, ws.err, d_pad, l_pad), gparams
+
+
+def grouped_fusable(L, d, k_group_size, nlut, seq_lens=None, scale_granularity="head"):
+    """The grouped-K fused kernel's domain: power-of-two groups of 8..128 keys that
+    tile L, d <= 128, LUTs of <= 64 entries, per-head Q/V, no per-batch lengths."""
+    gs = int(k_group_size)
+    return (8 <= gs <= 128 and gs & (gs - 1) == 0 and L % gs == 0 and d <= 128 and nlut <= 64
+            and seq_lens is None and scale_granularity == "head")
+
+
 def _finish_prepare(qhat, khat, vt, sq, sk, sv, ws, per_head, B, H, Hkv, d, b, c, p_scale, d_pad,
                     l_pad) -> Prepared:
     params = torch.empty((B * H, HEAD_PARAMS_BYTES), dtype=torch.uint8, device=qhat.device)
@@ -239,7 +286,8 @@ def _finish_prepare(qhat, khat, vt, sq, sk, sv, ws, per_head, B, H, Hkv, d, b, c
 
 
 def attn_fused(prep: Prepared, shape, out, *, causal=False, seq_lens=None, mask_bits=None,
-               lut=None, p_scale=255, debug=None, times=None, softmax_mode=_lib.IA_SOFTMAX_INDEX):
+               lut=None, p_scale=255, debug=None, times=None, softmax_mode=_lib.IA_SOFTMAX_INDEX,
+               kgroup=None, k_group_size=0):
     B, H, Hkv, Lq, d = shape
     a = _lib.AttnArgs()
     a.q, a.k, a.vt = prep.qhat.data_ptr(), prep.khat.data_ptr(), prep.vt.data_ptr()
@@ -260,6 +308,9 @@ def attn_fused(prep: Prepared, shape, out, *, causal=False, seq_lens=None, mask_
         a.dbg_acc = debug["acc"].data_ptr()
     if times is not None:
         a.dbg_times = times.data_ptr()
+    if kgroup is not None:
+        a.kgroup_params = kgroup.data_ptr()
+        a.k_group_size = int(k_group_size)
     _lib.check(_lib.load().ia_attn_fwd(ctypes.byref(a), _stream()), "attention")
 
 
@@ -275,7 +326,7 @@ def lut_bytes(b: int, c: float) -> np.ndarray:
 
 def attention(q, k, v, *, causal=False, seq_lens=None, mask=None, scale_granularity="head",
               b=5, c=6.6, p_scale=255, lut=None, out=None, debug=False, check_finite=True,
-              timer=None, scales=None, softmax="index"):
+              timer=None, scales=None, softmax="index", k_group_size=None):
     """Batched fused IntAttention on the current CUDA device.
 
     softmax="index" is IndexSoftmax (bit-exact with the reference); "float" runs
@@ -305,6 +356,12 @@ def attention(q, k, v, *, causal=False, seq_lens=None, mask=None, scale_granular
         raise ValueError("softmax must be 'index' or 'float'")
     if d_pad is None and softmax == "float":
         raise ValueError("the fused quant-only path needs head dim <= 256")
+    if k_group_size is not None and (d_pad is None or softmax != "index" or scales is not None
+                                     or not grouped_fusable(Lq, d, k_group_size, len(lut),
+                                                            seq_lens, scale_granularity)):
+        raise ValueError("grouped K in the fused kernel needs a power-of-two group of 8..128 "
+                         "keys dividing L, d <= 128, a <= 64-entry LUT, per-head Q/V scales "
+                         "and no seq_lens")
     if d_pad is None:
         if scales is not None:
             raise ValueError("precomputed scales need the fused path (head dim <= 256)")
@@ -315,8 +372,14 @@ def attention(q, k, v, *, causal=False, seq_lens=None, mask=None, scale_granular
             timer.mark("quantized")
             timer.mark("attention")
         return (res, {}) if debug else res
-    prep = prepare(q, k, v, seq_lens=seq_lens, scale_granularity=scale_granularity, b=b, c=c,
-                   p_scale=p_scale, d_pad=d_pad, scales=scales)
+    gparams = None
+    if k_group_size is not None:
+        # grouped K (per_row_group K scales; softmax.py:309-399, pipeline.py:229-246)
+        prep, gparams = prepare_grouped(q, k, v, k_group_size, b=b, c=c, p_scale=p_scale,
+                                        d_pad=d_pad)
+    else:
+        prep = prepare(q, k, v, seq_lens=seq_lens, scale_granularity=scale_granularity, b=b,
+                       c=c, p_scale=p_scale, d_pad=d_pad, scales=scales)
     mbits = pack_mask(mask) if mask is not None else None
     if timer is not None:
         timer.mark("quantized")
@@ -327,7 +390,8 @@ def attention(q, k, v, *, causal=False, seq_lens=None, mask=None, scale_granular
                "acc": torch.zeros((B * H, Lq, d_pad), dtype=torch.int32, device=q.device)}
     attn_fused(prep, (B, H, Hkv, Lq, d), out, causal=causal, seq_lens=seq_lens,
                mask_bits=mbits, lut=lut, p_scale=p_scale, debug=dbg,
-               softmax_mode=_lib.IA_SOFTMAX_FLOAT if softmax == "float" else _lib.IA_SOFTMAX_INDEX)
+               softmax_mode=_lib.IA_SOFTMAX_FLOAT if softmax == "float" else _lib.IA_SOFTMAX_INDEX,
+               kgroup=gparams, k_group_size=k_group_size or 0)
     if timer is not None:
         timer.mark("attention")
     if isinstance(check_finite, list):  # deferred: the caller checks after its pipeline

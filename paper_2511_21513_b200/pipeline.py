@@ -142,6 +142,11 @@ def int_attention(q, k, v, cfg=None, warmup=0, iters=1):
     lut = _sm.build_lut(cfg.b, cfg.c)
 
     if k_gran.kind == PER_ROW_GROUP:
+        k_gran.num_groups((n, d))  # group_size must divide L (quantize.py:46-56)
+        if E.pad_head_dim(d) is not None and E.grouped_fusable(n, d, k_gran.group_size,
+                                                               len(lut.entries)):
+            return _int_attention_grouped_fused(qt, kt, vt, mt, cfg, k_gran, lut, numpy_in,
+                                                warmup, iters)
         return _int_attention_grouped(qt, kt, vt, mt, cfg, k_gran, lut, numpy_in, warmup, iters)
 
     p_dt = np.int8 if cfg.p_format is PFormat.INT8X127 else np.uint8
@@ -167,9 +172,33 @@ def int_attention(q, k, v, cfg=None, warmup=0, iters=1):
     return to_host(out[0, 0], numpy_in), timings
 
 
+def _int_attention_grouped_fused(qt, kt, vt, mt, cfg, k_gran, lut, numpy_in, warmup, iters):
+    """Per-row-group K scales (pipeline.py:229-246) in ONE fused launch: the grouped
+    IndexSoftmax (softmax.py:309-399) runs between the two INT8 MMAs with a per-group
+    row max and clip threshold; logits never reach HBM (csrc/attention.cu, gk_passes)."""
+    p_dt = np.int8 if cfg.p_format is PFormat.INT8X127 else np.uint8
+
+    def once(clk):
+        # audit stream of the grouped path (softmax.py:394, :398, pipeline.py:248): the
+        # u8 surrogates and P^ the grouped kernel builds on chip
+        _sm._note("surrogates", np.uint8)
+        _sm._note("prob", p_dt)
+        _sm._note("pv_in", p_dt)
+        return E.attention(qt[None, None], kt[None, None], vt[None, None], mask=mt, b=cfg.b,
+                           c=cfg.c, p_scale=cfg.p_format.value, lut=lut.entries, timer=clk,
+                           k_group_size=k_gran.group_size)
+
+    out, timings = _run_measured(
+        once, warmup, iters,
+        {"quantize": ("start", "quantized"), "softmax_path": ("quantized", "attention"),
+         "total": ("start", "attention")})
+    return to_host(out[0, 0], numpy_in), timings
+
+
 def _int_attention_grouped(qt, kt, vt, mt, cfg, k_gran, lut, numpy_in, warmup, iters):
-    """Per-row-group K scales (pipeline.py:229-246): stage kernels + the grouped
-    IndexSoftmax composition."""
+    """Per-row-group K scales (pipeline.py:229-246) outside the fused kernel's domain
+    (group sizes that are not a power of two in [8, 128], d > 128): stage kernels + the
+    grouped IndexSoftmax row kernel."""
     from .gemm import gemm_pv, matmul_int8
     from .quantize import quantize_symmetric
 

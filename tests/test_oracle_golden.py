@@ -3,6 +3,8 @@
 The vectors were produced by importing the reference in the build container
 (oracle/gen_golden.py); nothing here reads /root/reference at run time.
 """
+import os
+
 import numpy as np
 import pytest
 
@@ -179,3 +181,16 @@ def test_oracle_quant_only_matches_reference():
                                            int(G[key + "_pf"]))
         assert np.array_equal(phat, G[key + "_phat"]), key
         assert np.array_equal(out.view(np.uint32), G[key + "_out"].view(np.uint32)), key
+
+
+def test_oracle_grouped_pipeline_vs_reference():
+    """The grouped-K oracle composition (oracle.attention_grouped_batched) reproduces the
+    reference's per-row-group K int_attention (pipeline.py:229-246) bit for bit on the
+    committed fixtures (gs 32, 16 and 7; causal and not)."""
+    G = np.load(os.path.join(os.path.dirname(__file__), "golden", "grouped_cases.npz"))
+    for i in range(int(G["n_pipe"])):
+        key = f"pipe{i}"
+        q, k, v = G[key + "_q"], G[key + "_k"], G[key + "_v"]
+        out = O.attention_grouped_batched(q[None, None], k[None, None], v[None, None],
+                                          int(G[key + "_gs"]), causal=bool(int(G[key + "_causal"])))
+        assert np.array_equal(out[0, 0].view(np.uint32), G[key + "_out"].view(np.uint32)), key

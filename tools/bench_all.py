@@ -23,7 +23,7 @@ from paper_2511_21513_b200 import engine as E  # noqa: E402
 from paper_2511_21513_b200 import workloads  # noqa: E402
 
 
-def run(name, iters, softmax="index"):
+def run(name, iters, softmax="index", k_group_size=None):
     G = configs().get(name)
     wl = workloads.make("C2" if name == "C2h" else name)
     gran = "head" if name == "C2h" else wl.scale_granularity
@@ -43,15 +43,16 @@ def run(name, iters, softmax="index"):
             e.record()
             self.ev[n] = e
 
-    E.attention(q, k, v, causal=wl.causal, seq_lens=sl, scale_granularity=gran, lut=lut, out=out, softmax=softmax)
+    E.attention(q, k, v, causal=wl.causal, seq_lens=sl, scale_granularity=gran, lut=lut, out=out, softmax=softmax,
+                k_group_size=k_group_size)
     for _ in range(3):
         E.attention(q, k, v, causal=wl.causal, seq_lens=sl, scale_granularity=gran, lut=lut,
-                    out=out, check_finite=False, softmax=softmax)
+                    out=out, check_finite=False, softmax=softmax, k_group_size=k_group_size)
     ts = []
     for _ in range(iters):
         t = T()
         E.attention(q, k, v, causal=wl.causal, seq_lens=sl, scale_granularity=gran, lut=lut,
-                    out=out, check_finite=False, timer=t, softmax=softmax)
+                    out=out, check_finite=False, timer=t, softmax=softmax, k_group_size=k_group_size)
         ts.append(t)
     torch.cuda.synchronize()
     tot = statistics.median(t.ev["start"].elapsed_time(t.ev["attention"]) for t in ts) / 1e3
@@ -59,7 +60,7 @@ def run(name, iters, softmax="index"):
     qnt = statistics.median(t.ev["start"].elapsed_time(t.ev["quantized"]) for t in ts) / 1e3
     res = out.cpu().numpy()
     exact = None
-    if G is not None and softmax == "index":
+    if G is not None and softmax == "index" and k_group_size is None:
         lens = wl.lengths()
         bad = 0
         u = 0
@@ -73,7 +74,7 @@ def run(name, iters, softmax="index"):
     ops = wl.ops()
     # algorithmic quantiser bytes over VALID rows only (pad rows are never read)
     qbytes = 5 * int(wl.lengths().sum()) * (H + 2 * Hkv) * d
-    return {"config": name, "softmax": softmax, "shape": [B, H, Hkv, L, d], "causal": wl.causal, "scale": gran,
+    return {"config": name, "softmax": softmax, "k_group_size": k_group_size, "shape": [B, H, Hkv, L, d], "causal": wl.causal, "scale": gran,
             "ms_total": tot * 1e3, "ms_quantize": qnt * 1e3, "ms_fused": att * 1e3,
             "tops_total": ops / tot / 1e12, "tops_fused": ops / att / 1e12,
             "tokens_per_s": wl.tokens() / tot, "quantizer_gbs": qbytes / qnt / 1e9,
@@ -87,10 +88,12 @@ def main():
     ap.add_argument("--iters", type=int, default=10)
     ap.add_argument("--softmax", default="index", choices=["index", "float", "both"],
                     help="float = the quant-only comparator mode of the fused kernel")
+    ap.add_argument("--k-group-size", type=int, default=None,
+                    help="grouped K (per-row-group key scales) in the fused kernel")
     a = ap.parse_args()
     for name in a.configs.split(","):
         for sm in (("index", "float") if a.softmax == "both" else (a.softmax,)):
-            print(json.dumps(run(name, a.iters, sm)), flush=True)
+            print(json.dumps(run(name, a.iters, sm, a.k_group_size)), flush=True)
 
 
 if __name__ == "__main__":
