@@ -7,26 +7,32 @@
 //     acc = P^ V^ (int32)                gemm.py:109-133
 //     out = f32(acc) * f32(s_v / 255)    pipeline.py:250-252
 // The int32 logits and the u8 probabilities never leave the SM: QK^T lands in
-// TMEM (tcgen05.mma kind::i8, s32 accumulate), the integer softmax reads it
-// back with tcgen05.ld, and P^ is written back into the same TMEM columns
-// (tcgen05.st) as the A operand of the P.V MMA.
+// TMEM (tcgen05.mma kind::i8, s32 accumulate), the integer softmax reads it back
+// with tcgen05.ld, and P^ goes to a K-major SWIZZLE_128B shared-memory tile that
+// is the A operand of the P.V MMA (SS form, u8 x s8 -> s32 in TMEM).
 //
-// IndexSoftmax needs the FINAL row max m (for delta = m - a) and the FINAL
-// integer row sum S (for the per-row table round(255 e / S)) before any P^ is
-// known, and its LUT values cannot be rescaled exactly, so the FlashAttention
-// running-max trick does not apply.  For more than two key tiles the kernel
-// therefore makes three passes over the key tiles, recomputing QK^T each pass:
-//   pass 1: row max;  pass 2: idx, S;  pass 3: P^ -> TMEM -> P.V MMA.
-// With <= 2 key tiles (L <= 256) the logits stay resident in TMEM and QK^T is
-// computed once.
+// IndexSoftmax needs the FINAL row max m (for delta = m - a) and the FINAL integer
+// row sum S (for the per-row table round(255 e / S)) before any P^ is known, and
+// its LUT values cannot be rescaled exactly, so the FlashAttention running-max
+// trick does not apply.  For more than NWG key tiles the kernel therefore makes
+// three passes over the key tiles, recomputing QK^T each pass:
+//   pass 1: row max (+ row min);  pass 2: idx, S;  pass 3: P^ -> smem -> P.V MMA.
+// With <= NWG key tiles (L <= 384 for d_pad <= 128) the logits stay resident in
+// TMEM and QK^T runs once.  Grouped K (per-row-group key scales, gk_passes) takes
+// its group maxima per tile and needs two passes.
 //
-// Warp roles (384 threads): warp 0 = TMA producer, warp 1 = MMA issuer,
-// warp 2 = TMEM allocator, warps 4-7 / 8-11 = softmax warpgroups 0 / 1.
-// Softmax warpgroup w owns key tiles n = w, w+2, ... and TMEM buffer S[w]
-// (128 lanes x 128 columns); each thread owns one query row (TMEM lane).
-// The two warpgroups merge their partial row max / row sum through smem.
+// Warps (512 threads for d_pad <= 128, 384 for 256): warps 0..4*NWG-1 are NWG = 3
+// (2) softmax warpgroups; the last four are the role warps -- K (+Q) TMA producer,
+// QK^T MMA issuer, V^T TMA producer + TMEM allocator, P.V MMA issuer -- at the
+// highest warp ids, which the scheduler favours.  Softmax warpgroup w owns key
+// tiles n = w, w+NWG, ... and TMEM buffer S[w] (128 lanes x 128 columns); each
+// thread owns one query row (TMEM lane).  The warpgroups merge their partial row
+// max / min / sum through smem at the pass boundaries.
 //
-// TMEM (512 columns): S[0] = cols [0,128), S[1] = [128,256), O = [256, 256+DP).
+// TMEM (512 columns): S[w] = cols [128w, 128w+128), O = [128 NWG, 128 NWG + DP).
+// SMEM: Q tile, K ring (NKST stages; in passes 1-2 the idle P^ area adds stages),
+// 2 V^T stages, NPB P^ tiles per warpgroup, the per-row normalisation tables, the
+// row exchange arrays and the mbarriers (see Cfg and DESIGN.md §5).
 #include <climits>
 #include <cstdint>
 #include <cstdlib>

@@ -9,7 +9,9 @@ and uint8 probabilities never touch HBM.
 Stage timings come from CUDA events.  Because QK^T, IndexSoftmax, P.V and the
 rescale are one kernel, ``StageTimings`` reports the quantiser in
 ``quantize_ns`` and the fused kernel in ``softmax_path_ns``; ``qk_gemm_ns``,
-``pv_gemm_ns`` and ``dequantize_ns`` are 0 (fused away).
+``pv_gemm_ns`` and ``dequantize_ns`` are 0 (fused away).  ``int_attention_staged``
+runs the same computation as the reference's five separate stages (bit-identical
+output) and reports every stage's time.
 """
 from __future__ import annotations
 
@@ -170,6 +172,71 @@ def int_attention(q, k, v, cfg=None, warmup=0, iters=1):
         {"quantize": ("start", "quantized"), "softmax_path": ("quantized", "attention"),
          "total": ("start", "attention")})
     return to_host(out[0, 0], numpy_in), timings
+
+
+def int_attention_staged(q, k, v, cfg=None, warmup=0, iters=1):
+    """``int_attention`` run as the reference's five stages, each its own launch
+    sequence, so ``StageTimings`` carries the full split the reference reports
+    (pipeline.py:61-81, 143-191, 215-253): quantize (3x quantize_symmetric), qk_gemm
+    (tcgen05 INT8 GEMM -> int32 logits in HBM), softmax_path (LUT, c_int and the
+    IndexSoftmax row kernel -> u8 P^ in HBM), pv_gemm (tcgen05 GEMM -> int32) and
+    dequantize (f32 rescale).  A debug / analysis mode: the logits and P^ round-trip
+    through HBM here, which the fused ``int_attention`` never does.  The output is
+    bit-identical to ``int_attention``; the per-stage times explain the fused one."""
+    from .gemm import gemm_pv, gemm_qk, matmul_int8
+    from .quantize import quantize_symmetric
+
+    cfg = cfg or AttentionConfig()
+    n, d = _check_inputs(q, k, v)
+    mask = _check_mask(cfg.mask, n)
+    k_gran = _k_granularity(cfg)
+    numpy_in = not is_torch(q)
+    qt, kt, vt = (to_device(x, np.float32) for x in (q, k, v))
+    mt = to_device(mask).to(torch.bool) if mask is not None else None
+
+    def once(clk):
+        if clk:
+            clk.mark("start")
+        qh = quantize_symmetric(qt)
+        kh = quantize_symmetric(kt, k_gran)
+        vh = quantize_symmetric(vt)
+        if clk:
+            clk.mark("quantized")
+        if k_gran.kind == PER_TENSOR:
+            lm = gemm_qk(qh, kh)
+            logits = lm.values
+        else:
+            logits = matmul_int8(qh.values, kh.values)
+        if clk:
+            clk.mark("qk")
+        lut = _sm.build_lut(cfg.b, cfg.c)
+        if k_gran.kind == PER_TENSOR:
+            ci = _sm.compute_c_int(cfg.c, d, float(qh.scales[0]), float(kh.scales[0]))
+            prob = _sm.index_softmax(logits, ci, lut, mask=mt, p_format=cfg.p_format)
+        else:
+            s_q = float(qh.scales[0])
+            alphas = [s_q * float(sk) / math.sqrt(d) for sk in kh.scales.tolist()]
+            groups = np.repeat(np.arange(len(alphas)), k_gran.group_size)
+            prob = _sm.index_softmax_grouped(logits, groups, alphas, cfg.c, lut, mask=mt,
+                                             p_format=cfg.p_format)
+        if clk:
+            clk.mark("softmax")
+        _sm._note("pv_in", prob.values)
+        acc = gemm_pv(prob.values, vh)
+        if clk:
+            clk.mark("pv")
+        out = acc.to(torch.float32) * torch.tensor(
+            np.float32(float(vh.scales[0]) / prob.denom_scale), device=qt.device)
+        if clk:
+            clk.mark("end")
+        return out
+
+    out, timings = _run_measured(
+        once, warmup, iters,
+        {"quantize": ("start", "quantized"), "qk_gemm": ("quantized", "qk"),
+         "softmax_path": ("qk", "softmax"), "pv_gemm": ("softmax", "pv"),
+         "dequantize": ("pv", "end"), "total": ("start", "end")})
+    return to_host(out, numpy_in), timings
 
 
 def _int_attention_grouped_fused(qt, kt, vt, mt, cfg, k_gran, lut, numpy_in, warmup, iters):
