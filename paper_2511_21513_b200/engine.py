@@ -405,6 +405,37 @@ def attention(q, k, v, *, causal=False, seq_lens=None, mask=None, scale_granular
     return out
 
 
+class AttentionGraph:
+    """One ``attention`` call on fixed device tensors, captured once into a CUDA graph
+    and replayed: the workspace fill, the quantiser, the parameter and the fused
+    launches go to the GPU as one graph launch with no host work between them (for
+    small problems -- C1, C2 -- the host-side launch sequence is a large part of a
+    call).  ``replay()`` recomputes ``out`` from the current contents of q, k, v.
+    The non-finite check is not part of the graph (``check()`` reads the flag)."""
+
+    def __init__(self, q, k, v, out, **kw):
+        kw = dict(kw, out=out, check_finite=[])
+        attention(q, k, v, **kw)  # eager warm-up: validation, tensor maps, smem attributes
+        torch.cuda.synchronize()
+        self.graph = torch.cuda.CUDAGraph()
+        side = torch.cuda.Stream()
+        side.wait_stream(torch.cuda.current_stream())
+        flags = []
+        with torch.cuda.stream(side), torch.cuda.graph(self.graph, stream=side):
+            attention(q, k, v, **dict(kw, check_finite=flags))
+        torch.cuda.current_stream().wait_stream(side)
+        self._flags = flags
+        self.out = out
+
+    def replay(self):
+        self.graph.replay()
+        return self.out
+
+    def check(self):
+        for f in self._flags:
+            raise_if_nonfinite(f)
+
+
 def gemm_i8(a, b_t, *, a_signed=True):
     """C = a @ b_t^T (int32) on tcgen05.  a [M, K] int8/uint8, b_t [N, K] int8 (CUDA)."""
     M, K = a.shape

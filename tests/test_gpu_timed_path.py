@@ -67,3 +67,26 @@ def test_out_argument_validated():
             E.attention(q, k, k, out=bad)
     good = torch.empty(1, 2, 64, 32, device=dev)
     assert E.attention(q, k, k, out=good) is good
+
+
+def test_attention_graph_replay_bit_exact_and_live_inputs():
+    """engine.AttentionGraph: the captured call equals the eager one, and a replay
+    after new data is written into the same input tensors recomputes from it."""
+    from oracle import oracle as O
+    rng = np.random.default_rng(17)
+    dev = torch.device("cuda", 0)
+    shape_q, shape_k = (2, 4, 200, 64), (2, 2, 200, 64)
+    q, k, v = (torch.from_numpy(rng.standard_normal(s, dtype=np.float32)).to(dev)
+               for s in (shape_q, shape_k, shape_k))
+    out = torch.empty_like(q)
+    g = E.AttentionGraph(q, k, v, out, causal=True)
+    for _ in range(2):
+        g.replay()
+    g.check()
+    want, _ = O.attention_batched(q.cpu().numpy(), k.cpu().numpy(), v.cpu().numpy(), causal=True)
+    assert np.array_equal(out.cpu().numpy().view(np.uint32), want.view(np.uint32))
+    for t, s in ((q, shape_q), (k, shape_k), (v, shape_k)):
+        t.copy_(torch.from_numpy(rng.standard_normal(s, dtype=np.float32)))
+    g.replay()
+    want, _ = O.attention_batched(q.cpu().numpy(), k.cpu().numpy(), v.cpu().numpy(), causal=True)
+    assert np.array_equal(out.cpu().numpy().view(np.uint32), want.view(np.uint32))

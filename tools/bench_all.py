@@ -23,7 +23,7 @@ from paper_2511_21513_b200 import engine as E  # noqa: E402
 from paper_2511_21513_b200 import workloads  # noqa: E402
 
 
-def run(name, iters, softmax="index", k_group_size=None):
+def run(name, iters, softmax="index", k_group_size=None, graph=False):
     G = configs().get(name)
     wl = workloads.make("C2" if name == "C2h" else name)
     gran = "head" if name == "C2h" else wl.scale_granularity
@@ -56,6 +56,20 @@ def run(name, iters, softmax="index", k_group_size=None):
         ts.append(t)
     torch.cuda.synchronize()
     tot = statistics.median(t.ev["start"].elapsed_time(t.ev["attention"]) for t in ts) / 1e3
+    graph_ms = None
+    if graph:  # the same call replayed from a CUDA graph (no host gaps between launches)
+        G_ = E.AttentionGraph(q, k, v, out, causal=wl.causal, seq_lens=sl, scale_granularity=gran,
+                              lut=lut, softmax=softmax, k_group_size=k_group_size)
+        for _ in range(3):
+            G_.replay()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(iters):
+            G_.replay()
+        e1.record()
+        torch.cuda.synchronize()
+        graph_ms = e0.elapsed_time(e1) / iters
+        G_.check()
     att = statistics.median(t.ev["quantized"].elapsed_time(t.ev["attention"]) for t in ts) / 1e3
     qnt = statistics.median(t.ev["start"].elapsed_time(t.ev["quantized"]) for t in ts) / 1e3
     res = out.cpu().numpy()
@@ -76,6 +90,7 @@ def run(name, iters, softmax="index", k_group_size=None):
     qbytes = 5 * int(wl.lengths().sum()) * (H + 2 * Hkv) * d
     return {"config": name, "softmax": softmax, "k_group_size": k_group_size, "shape": [B, H, Hkv, L, d], "causal": wl.causal, "scale": gran,
             "ms_total": tot * 1e3, "ms_quantize": qnt * 1e3, "ms_fused": att * 1e3,
+            "ms_step_graph": graph_ms,
             "tops_total": ops / tot / 1e12, "tops_fused": ops / att / 1e12,
             "tokens_per_s": wl.tokens() / tot, "quantizer_gbs": qbytes / qnt / 1e9,
             "bit_exact_vs_reference": exact,
@@ -88,12 +103,14 @@ def main():
     ap.add_argument("--iters", type=int, default=10)
     ap.add_argument("--softmax", default="index", choices=["index", "float", "both"],
                     help="float = the quant-only comparator mode of the fused kernel")
+    ap.add_argument("--graph", action="store_true",
+                    help="also time the step replayed from a CUDA graph")
     ap.add_argument("--k-group-size", type=int, default=None,
                     help="grouped K (per-row-group key scales) in the fused kernel")
     a = ap.parse_args()
     for name in a.configs.split(","):
         for sm in (("index", "float") if a.softmax == "both" else (a.softmax,)):
-            print(json.dumps(run(name, a.iters, sm, a.k_group_size)), flush=True)
+            print(json.dumps(run(name, a.iters, sm, a.k_group_size, a.graph)), flush=True)
 
 
 if __name__ == "__main__":
