@@ -551,9 +551,8 @@ def run_sharded(args, wl_name, compute=None):
 
         def step(timer=None):
             sc = None
-            if gran == "tensor":  # all-reduce(MAX) of the 3 local amax values (NCCL)
-                s3 = sharding.global_scales(qd, kd, vd, sl, world=world)
-                sc = tuple(torch.tensor([s], dtype=torch.float32, device=dev) for s in s3)
+            if gran == "tensor":  # all-reduce(MAX) of the 3 local amax values (NCCL, on device)
+                sc = sharding.global_scales(qd, kd, vd, sl, world=world, device_out=True)
             if mine:
                 E.attention(qd, kd, vd, causal=wl.causal, seq_lens=sl_d,
                             scale_granularity="tensor" if sc else gran, lut=lut, out=out_d,
@@ -566,11 +565,10 @@ def run_sharded(args, wl_name, compute=None):
         if mine:
             E.attention(qd, kd, vd, causal=wl.causal, seq_lens=sl_d, scale_granularity=gran,
                         lut=lut, out=out_d, check_finite=True,
-                        scales=None if gran != "tensor" else tuple(
-                            torch.tensor([s], dtype=torch.float32, device=dev)
-                            for s in sharding.global_scales(qd, kd, vd, sl, world=world)))
+                        scales=None if gran != "tensor" else
+                        sharding.global_scales(qd, kd, vd, sl, world=world, device_out=True))
         elif gran == "tensor":
-            sharding.global_scales(None, None, None, None, world=world)
+            sharding.global_scales(None, None, None, None, world=world, device_out=True)
         for _ in range(args.warmup):
             step()
         torch.cuda.synchronize()
@@ -718,6 +716,9 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-comparator", action="store_true",
                     help="skip timing the quant-only comparator mode")
+    ap.add_argument("--sharded", action="store_true",
+                    help="run the N-rank sharded path even at N = 1 (exercises the NCCL "
+                         "launcher on a single GPU)")
     ap.add_argument("--compute", default=None,
                     help="module:function replacing the device compute of the N-rank path "
                          "(gloo; CPU tests of the launcher only)")
@@ -728,7 +729,7 @@ def main():
         return spawn(args)
     if args.impl == "reference":
         return run_reference(args, args.workload)
-    if _env_int("WORLD_SIZE", 1) > 1 or args.compute:
+    if _env_int("WORLD_SIZE", 1) > 1 or args.compute or args.sharded:
         return run_sharded(args, args.workload, compute=args.compute)
     return run_gpu(args, args.workload)
 

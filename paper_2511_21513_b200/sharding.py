@@ -145,29 +145,53 @@ def _local_amax_host(x, sl):
     return best
 
 
-def _local_amax_device(x, sl):
+def _local_amax_device(x, sl, amax_bits, err):
     """max|x| over the valid rows of every packed group with the library's amax
-    kernel (float bits, exact); returns a 1-element f32 CUDA tensor."""
+    kernel (float bits, exact) into the 1-element int32 slot ``amax_bits``."""
     from . import engine as E
     n, g, L, d = x.shape
-    buf = torch.zeros(2, dtype=torch.int32, device=x.device)
     slt = None if sl is None else torch.as_tensor(sl, dtype=torch.int32).to(x.device)
-    E.amax_rows(x.contiguous(), n * g, L, d, buf[:1], buf[1:], seq_lens=slt, valid_div=g,
+    E.amax_rows(x.contiguous(), n * g, L, d, amax_bits, err, seq_lens=slt, valid_div=g,
                 slot_div=n * g)
-    E.raise_if_nonfinite(buf[1:])
-    return buf[:1].view(torch.float32)
 
 
-def global_scales(qs, ks, vs, sl, group=None, world=1):
+def global_scales(qs, ks, vs, sl, group=None, world=1, device_out=False):
     """Global per-tensor scales of a sharded batch: every rank contributes the amax
-    of the rows it owns, all-reduce(MAX) of 3 floats on the collective device, then
-    s = max(amax, 1e-12) / 127 in f32 (quantize.py:113).  Returns 3 f32 scales
-    (numpy scalars)."""
+    of the rows it owns, all-reduce(MAX) of 3 values on the collective device, then
+    s = max(amax, 1e-12) / 127 in f32 (quantize.py:113).
+
+    CUDA inputs (NCCL): the amax kernel writes the float bits of the three local
+    maxima (non-negative floats order as their int32 bits), NCCL all-reduces them
+    with MAX and the library's scales kernel turns them into scales -- no host round
+    trip; with ``device_out`` the three scales come back as 1-element f32 CUDA
+    tensors (what ``engine.attention(scales=...)`` takes).  Host inputs (gloo):
+    numpy amax, host all-reduce, numpy f32 scales."""
     cdev = collective_device(group)
+    if isinstance(qs, torch.Tensor) and qs.is_cuda and cdev.type == "cuda" or (
+            qs is None and cdev.type == "cuda"):
+        from . import engine as E
+        buf = torch.zeros(4, dtype=torch.int32, device=cdev)
+        if qs is not None:
+            for t, x in enumerate((qs, ks, vs)):
+                _local_amax_device(x, sl, buf[t:t + 1], buf[3:])
+            E.raise_if_nonfinite(buf[3:])
+        amax = buf[:3]
+        if world > 1:
+            dist.all_reduce(amax, op=dist.ReduceOp.MAX, group=group)
+        sc = torch.empty(3, dtype=torch.float32, device=cdev)
+        E.scales_from_amax(amax, sc)
+        if device_out:
+            return tuple(sc[t:t + 1] for t in range(3))
+        return tuple(np.float32(x) for x in sc.cpu().numpy())
     if qs is None:
         local = torch.zeros(3, dtype=torch.float32)
-    elif isinstance(qs, torch.Tensor) and qs.is_cuda:
-        local = torch.cat([_local_amax_device(x, sl) for x in (qs, ks, vs)])
+    elif isinstance(qs, torch.Tensor) and qs.is_cuda:  # CUDA data under gloo
+        from . import engine as E
+        buf = torch.zeros(4, dtype=torch.int32, device=qs.device)
+        for t, x in enumerate((qs, ks, vs)):
+            _local_amax_device(x, sl, buf[t:t + 1], buf[3:])
+        E.raise_if_nonfinite(buf[3:])
+        local = buf[:3].view(torch.float32).cpu()
     else:
         local = torch.tensor([_local_amax_host(x, sl) for x in (qs, ks, vs)], dtype=torch.float32)
     local = local.to(cdev)
@@ -209,10 +233,16 @@ def gather_blocks(local_out, ranks, rank, shape, g, *, group=None, gather_to=0, 
         dist.gather(blk, parts, dst=gather_to, group=group)
         if not recv:
             return None
+    # one indexed copy places every rank's groups: group (b, kvh) -> out[b, kvh*G:(kvh+1)*G]
+    Hkv = H // G
+    src = [r * max_n + u for r, grs in enumerate(ranks) for u in range(len(grs))]
+    dst = [gr.b * Hkv + gr.kvh for grs in ranks for gr in grs]
+    blocks = torch.cat(parts) if len(parts) > 1 else parts[0]
+    if src != list(range(len(src))):  # ranks hold fewer than max_n groups: compact first
+        blocks = blocks[torch.as_tensor(src, device=cdev)]
     out = torch.empty((B, H, L, d), dtype=torch.float32, device=cdev)
-    for r, grs in enumerate(ranks):
-        for u, gr in enumerate(grs):
-            out[gr.b, gr.kvh * G:(gr.kvh + 1) * G] = parts[r][u]
+    out.view(B * Hkv, G, L, d).index_copy_(0, torch.as_tensor(dst, device=cdev),
+                                            blocks[:len(src)])
     if cdev.type == "cuda" or isinstance(like, torch.Tensor):
         return out
     return out.numpy()
