@@ -1,4 +1,6 @@
 #!/bin/bash
+# Needs the instrumented build (the release library ignores these knobs):
+#   make -C paper_2511_21513_b200/csrc profile; export IA_LIB=paper_2511_21513_b200/_lib/libintattn_b200_prof.so
 # A/B device time of the old/new library builds under IA_XFLAGS values (development tool).
 #   tools/abx.sh CONFIGS "xflags..." [rounds]
 cfg=${1:-C4}; xs=${2:-0}; rounds=${3:-1}

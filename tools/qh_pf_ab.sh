@@ -1,4 +1,6 @@
 # A/B of the quantiser's next-slab L2 prefetch (IA_QH_PF) across L2 budgets, then the
+# Needs the instrumented build (the release library ignores these knobs):
+#   make -C paper_2511_21513_b200/csrc profile; export IA_LIB=paper_2511_21513_b200/_lib/libintattn_b200_prof.so
 # GPU parity tests with the prefetch on.  Run on the GPU box from the repo root.
 set -x
 for pf in 0 1; do for l2 in 32 48 64; do

@@ -1,4 +1,6 @@
 #!/bin/bash
+# Needs the instrumented build (the release library ignores these knobs):
+#   make -C paper_2511_21513_b200/csrc profile; export IA_LIB=paper_2511_21513_b200/_lib/libintattn_b200_prof.so
 # Device time of the fused kernel under IA_XFLAGS experiment bits (development tool).
 #   tools/xflags.sh CONFIGS "0 1 2 ..."
 cfg=${1:-C4}
