@@ -38,6 +38,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <type_traits>
+#include <utility>
 
 #include "common.cuh"
 #include "params.cuh"
@@ -100,7 +101,10 @@ struct Cfg {
   // regular stages; every pass-2 QK^T has completed (its S tile was read) before
   // any warpgroup leaves the pass-2 row-sum exchange and writes a P^ tile.
   static constexpr int NKX_RAW = NKST + (NWG * NPB * P_BYTES) / K_BYTES;
-  static constexpr int NKX = NKX_RAW > 16 ? 16 : NKX_RAW;
+  // ring sizes are multiples of NWG so that, with the ring restarting at stage 0 every
+  // pass (IA_QK_UNROLL), stage ks of a pass always feeds buffer ks % NWG
+  static constexpr int NKX = ((NKX_RAW > 16 ? 16 : NKX_RAW) / NWG) * NWG;
+  static_assert(NKST % NWG == 0 && NKX % NWG == 0 && NKX >= NKST, "K ring sizes");
   static constexpr int KSTEPS = DP / 32;
   static constexpr int BAR_BYTES = 8 * (1 + 2 * NKX + 2 * NVST + 2 * NWG + 2 * NWG * NPB + 1) + 4;
   static_assert(BAR_BYTES <= 512, "barrier block");
@@ -131,6 +135,19 @@ __device__ __forceinline__ uint32_t chunk_mask(const AttnDev& p, int i, int j0, 
   if (j0 + 31 > lim) mb = (lim < j0) ? 0xffffffffu : (0xfffffffeu << (lim - j0));
   if (p.mask_bits && j0 < p.L) mb |= __ldg(p.mask_bits + (size_t)i * p.mask_words + (j0 >> 5));
   return mb;
+}
+
+__host__ __device__ constexpr int gcd_i(int a, int b) { return b ? gcd_i(b, a % b) : a; }
+__host__ __device__ constexpr int lcm_i(int a, int b) { return a / gcd_i(a, b) * b; }
+
+// f(std::integral_constant<int, 0>{}) ... f(std::integral_constant<int, N - 1>{})
+template <class F, int... I>
+__device__ __forceinline__ void static_for_impl(F&& f, std::integer_sequence<int, I...>) {
+  (f(std::integral_constant<int, I>{}), ...);
+}
+template <int N, class F>
+__device__ __forceinline__ void static_for(F&& f) {
+  static_for_impl(f, std::make_integer_sequence<int, N>{});
 }
 
 __device__ __forceinline__ uint32_t lds_u8(uint32_t addr) {
@@ -198,6 +215,15 @@ __device__ __forceinline__ void bwait(uint64_t* bar, uint32_t parity, bool spin)
 //   IA_ISSUER_BACKOFF_NS   MMA issuers likewise
 #ifndef IA_ROLE_FIRST
 #define IA_ROLE_FIRST 0
+#endif
+// QK^T issuer unrolled over the K ring (stage / buffer indices compile-time); the K
+// ring then restarts at stage 0 every pass (producer and issuer alike)
+#ifndef IA_QK_UNROLL
+#define IA_QK_UNROLL 1
+#endif
+// the same for the P.V issuer (measured 0.7 % slower on C4: off)
+#ifndef IA_PV_UNROLL
+#define IA_PV_UNROLL 0
 #endif
 #ifndef IA_PRODUCER_BACKOFF_NS
 #define IA_PRODUCER_BACKOFF_NS 0
@@ -579,9 +605,12 @@ __global__ void __launch_bounds__(Cfg<DP>::NTHREADS, 1)
                       n * BN, kvh);
       }
       __syncwarp();
-      if (++n == n_kt) n = 0;
       ++ks;
       if (t + 1 < t3 ? ks == C::NKX : ks == C::NKST) ks = 0;
+      if (++n == n_kt) {
+        n = 0;
+        if (IA_QK_UNROLL) ks = 0;  // every pass starts at stage 0
+      }
       if (t + 1 == t3) ks = 0;
     }
   } else if (rw == 2) {
@@ -606,10 +635,51 @@ __global__ void __launch_bounds__(Cfg<DP>::NTHREADS, 1)
     mbar_wait(q_full, 0);
     uint32_t kph = 0;            // per-stage K phase bits
     uint32_t used = 0, c_s = 0;  // per-buffer occupied bit / s_free phase
-    int w = 0, n = 0, ks = 0;
-    const int t3 = PV_PASS * n_kt;
-    const int nmma = npass * n_kt;
-    for (int t = 0; t < nmma; ++t) {
+#if IA_QK_UNROLL
+    // one pass at a time; within a pass tile n uses K stage n % RING and buffer n % NWG,
+    // so an unrolled round over the ring has every barrier, descriptor and TMEM column
+    // offset as a compile-time constant
+    const uint32_t tm = *tmem_slot;  // re-read: keeps the loop free of a spilled reload
+    auto qk_tile = [&](auto J) {
+      constexpr int ks = decltype(J)::value;
+      constexpr int w = ks % NWG;
+      const bool need_free = (used >> w) & 1u;
+      const uint32_t f_ok = need_free ? mbar_test(s_free + w, (c_s >> w) & 1u) : 1u;
+      const uint32_t k_ok = mbar_test(k_full + ks, (kph >> ks) & 1u);
+      if (!f_ok) iwait(s_free + w, (c_s >> w) & 1u, XF(2));
+      if (need_free) c_s ^= 1u << w;
+      used |= 1u << w;
+      if (!k_ok) iwait(k_full + ks, (kph >> ks) & 1u, XF(2));
+      kph ^= 1u << ks;
+      tc_fence_after();
+      if (elect_one()) {
+        const uint64_t dk = d0 + (uint64_t)(C::k_off(ks) >> 4);
+#pragma unroll
+        for (int kk = 0; kk < C::KSTEPS; ++kk) {
+          const uint32_t off = (kk * 32 / C::SW) * C::SUB_BYTES + (kk * 32) % C::SW;
+          mma_i8_ss(tm + (uint32_t)w * 128u, dq + (off >> 4), dk + (off >> 4), idq, kk > 0);
+        }
+        tc_commit(k_empty + ks);
+        tc_commit(s_full + w);
+      }
+      __syncwarp();
+    };
+    for (int pass = 0; pass < (resident ? 0 : npass); ++pass) {  // resident: generic loop
+      if (pass < PV_PASS) {
+        for (int n0 = 0; n0 < n_kt; n0 += C::NKX)
+          static_for<C::NKX>([&](auto J) {
+            if (n0 + decltype(J)::value < n_kt) qk_tile(J);
+          });
+      } else {
+        for (int n0 = 0; n0 < n_kt; n0 += C::NKST)
+          static_for<C::NKST>([&](auto J) {
+            if (n0 + decltype(J)::value < n_kt) qk_tile(J);
+          });
+      }
+    }
+    if (resident)
+#endif
+    for (int t = 0, w = 0, n = 0, ks = 0, t3 = PV_PASS * n_kt; t < npass * n_kt; ++t) {
       long long t0 = clk64();
       if (lane == 0) IA_TRACE(1, 2, t);
       // both readiness tests in flight at once; block only on what is not ready yet
@@ -642,9 +712,12 @@ __global__ void __launch_bounds__(Cfg<DP>::NTHREADS, 1)
       }
       __syncwarp();
       if (++w == NWG) w = 0;
-      if (++n == n_kt) { n = 0; w = 0; }
       ++ks;
       if (t + 1 < t3 ? ks == C::NKX : ks == C::NKST) ks = 0;
+      if (++n == n_kt) {
+        n = 0;
+        w = 0;
+      }
       if (t + 1 == t3) ks = 0;
     }
   } else if (rw == 3) {
@@ -652,8 +725,42 @@ __global__ void __launch_bounds__(Cfg<DP>::NTHREADS, 1)
     constexpr uint32_t idv = idesc_i8(BM, DP, false, true);  // u8 x s8 -> s32
     const uint64_t dp0 = sdesc(smem_u32(smem + C::OFF_P), 1024, 2u);
     const uint64_t dv0 = sdesc(smem_u32(smem + C::OFF_V), 1024, 2u);
+#if IA_PV_UNROLL
+    // unrolled over one period of (P^ buffer, V^T stage): tile n uses P^ buffer
+    // (n % NWG) * NPB + (n / NWG) % NPB and V^T stage n % NVST -- compile-time in a round
+    if (!resident) {
+      constexpr int PER = lcm_i(NWG * C::NPB, C::NVST);
+      static_assert(PER % C::NVST == 0 && PER % (NWG * C::NPB) == 0, "P.V unroll period");
+      const uint32_t tm = *tmem_slot;
+      uint32_t pph = 0, vph2 = 0;  // P^ round parity, V^T phase bits per stage
+      for (int n0 = 0; n0 < n_kt_b; n0 += PER) {
+        static_for<PER>([&](auto J) {
+          constexpr int j = decltype(J)::value;
+          constexpr int pb = (j % NWG) * C::NPB + (j / NWG) % C::NPB;
+          constexpr int vs = j % C::NVST;
+          if (n0 + j >= n_kt_b) return;
+          iwait(p_full + pb, (pph ^ (uint32_t)((j / (NWG * C::NPB)) & 1)) & 1u, XF(8));
+          iwait(v_full + vs, (vph2 >> vs) & 1u, XF(8));
+          vph2 ^= 1u << vs;
+          tc_fence_after();
+          if (elect_one()) {
+            const uint64_t dp = dp0 + (uint64_t)((pb * C::P_BYTES) >> 4);
+            const uint64_t dv = dv0 + (uint64_t)((vs * C::V_BYTES) >> 4);
+#pragma unroll
+            for (int kk = 0; kk < BN / 32; ++kk)
+              mma_i8_ss(tm + C::O_COL, dp + 2 * kk, dv + 2 * kk, idv,
+                        (n0 + j > 0 || kk > 0) ? 1u : 0u);
+            tc_commit(v_empty + vs);
+            tc_commit(p_free + pb);
+          }
+          __syncwarp();
+        });
+        pph ^= (uint32_t)((PER / (NWG * C::NPB)) & 1);
+      }
+    }
+#endif
     int vs = 0, vph = 0, w = 0, tl = 0;  // warpgroup w's local tile counter tl
-    for (int n = 0; n < n_kt_b; ++n) {
+    for (int n = 0; n < ((IA_PV_UNROLL && !resident) ? 0 : n_kt_b); ++n) {
       const int pb = w * C::NPB + tl % C::NPB;
       long long t0 = clk64();
       iwait(p_full + pb, (uint32_t)(tl / C::NPB) & 1u, XF(8));
