@@ -640,17 +640,22 @@ __global__ void __launch_bounds__(Cfg<DP>::NTHREADS, 1)
     // so an unrolled round over the ring has every barrier, descriptor and TMEM column
     // offset as a compile-time constant
     const uint32_t tm = *tmem_slot;  // re-read: keeps the loop free of a spilled reload
+    // s_free parity starts at 1: a fresh barrier counts its (nonexistent) previous
+    // phase as complete, so every buffer's first use passes without a special case
+    uint32_t f_ph = (1u << NWG) - 1u;
     auto qk_tile = [&](auto J) {
       constexpr int ks = decltype(J)::value;
       constexpr int w = ks % NWG;
-      const bool need_free = (used >> w) & 1u;
-      const uint32_t f_ok = need_free ? mbar_test(s_free + w, (c_s >> w) & 1u) : 1u;
+      const long long t0 = clk64();
+      const uint32_t f_ok = mbar_test(s_free + w, (f_ph >> w) & 1u);
       const uint32_t k_ok = mbar_test(k_full + ks, (kph >> ks) & 1u);
-      if (!f_ok) iwait(s_free + w, (c_s >> w) & 1u, XF(2));
-      if (need_free) c_s ^= 1u << w;
-      used |= 1u << w;
+      if (!f_ok) iwait(s_free + w, (f_ph >> w) & 1u, XF(2));
+      f_ph ^= 1u << w;
+      const long long t1 = clk64();
       if (!k_ok) iwait(k_full + ks, (kph >> ks) & 1u, XF(2));
       kph ^= 1u << ks;
+      IA_TADD(8, t1 - t0);
+      IA_TADD(9, clk64() - t1);
       tc_fence_after();
       if (elect_one()) {
         const uint64_t dk = d0 + (uint64_t)(C::k_off(ks) >> 4);
