@@ -225,6 +225,10 @@ __device__ __forceinline__ void bwait(uint64_t* bar, uint32_t parity, bool spin)
 #ifndef IA_PV_UNROLL
 #define IA_PV_UNROLL 0
 #endif
+// pass-3 16-key group skip below the row's nonzero threshold (rows of >= 16 key tiles)
+#ifndef IA_GROUP_SKIP
+#define IA_GROUP_SKIP 1
+#endif
 #ifndef IA_PRODUCER_BACKOFF_NS
 #define IA_PRODUCER_BACKOFF_NS 0
 #endif
@@ -1132,14 +1136,16 @@ __global__ void __launch_bounds__(Cfg<DP>::NTHREADS, 1)
             // table).  Groups of 16 keys below every row's threshold stay zero.
             const uint32_t nk2 = im.nk2, base = im.base;
             const int32_t lo = im.lo;
-            auto groups = [&](auto clip) {
+            auto groups = [&](auto clip, auto skip) {
 #pragma unroll
               for (int g = 0; g < 4; ++g) {
                 const uint32_t* v16 = g < 2 ? &va[16 * g] : &vb[16 * (g - 2)];
-                int32_t gm = (int32_t)v16[0];
+                if (decltype(skip)::value) {
+                  int32_t gm = (int32_t)v16[0];
 #pragma unroll
-                for (int e = 1; e < 16; ++e) gm = max(gm, (int32_t)v16[e]);
-                if (!__any_sync(0xffffffffu, gm >= theta)) continue;  // pk stays 0
+                  for (int e = 1; e < 16; ++e) gm = max(gm, (int32_t)v16[e]);
+                  if (!__any_sync(0xffffffffu, gm >= theta)) continue;  // pk stays 0
+                }
 #pragma unroll
                 for (int q = 0; q < 4; ++q) {
                   const uint32_t* v4 = v16 + 4 * q;
@@ -1155,8 +1161,16 @@ __global__ void __launch_bounds__(Cfg<DP>::NTHREADS, 1)
                 }
               }
             };
-            if (uncl3) groups(std::false_type{});
-            else groups(std::true_type{});
+            // short rows (theta = INT_MIN) take the branch-free form: all 64 logits
+            // interleave freely
+            const bool skip = IA_GROUP_SKIP && n_kt >= 16;
+            if (uncl3) {
+              if (skip) groups(std::false_type{}, std::true_type{});
+              else groups(std::false_type{}, std::false_type{});
+            } else {
+              if (skip) groups(std::true_type{}, std::true_type{});
+              else groups(std::true_type{}, std::false_type{});
+            }
           } else if (!any_cut) {
 #pragma unroll
             for (int q = 0; q < 16; ++q) {
