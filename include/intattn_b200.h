@@ -19,8 +19,9 @@
 extern "C" {
 #endif
 
-#define IA_ABI_VERSION 4  /* 2: ia_head_params gained magic9; 3: ia_attn_args.softmax_mode;
-                            4: grouped-K fields of ia_attn_args, ia_group_params */
+#define IA_ABI_VERSION 5  /* 2: ia_head_params gained magic9; 3: ia_attn_args.softmax_mode;
+                            4: grouped-K fields of ia_attn_args, ia_group_params;
+                            5: ia_head_params.fratio (in the struct's former tail padding) */
 #define IA_MAX_SEQ_LEN 65536   /* gemm.py:26 MAX_SEQ_LEN */
 #define IA_MAX_HEAD_DIM 131070 /* gemm.py:25 MAX_HEAD_DIM */
 #define IA_FUSED_MAX_HEAD_DIM 256
@@ -122,6 +123,8 @@ typedef struct ia_head_params {
   float s_q, s_k, s_v;
   int32_t unc32;    /* 1: the magic is also exact without the clip (n up to 2k*2*d*127^2 + c_eff) */
   uint32_t magic9;  /* 0, or: idx * 512 = umulhi(n, magic9) & ~511 for the clipped n range */
+  float fratio;     /* 0, or the smallest f32 above k / c_eff (c_eff < 2^23): the float form
+                     * idx = RN(delta * fratio) is exact while c_eff (2 idx_max + 1) < 2^23 */
 } ia_head_params;
 
 int ia_head_params_host(double c, int64_t d, int nlut, int p_scale, float s_q, float s_k,

@@ -42,7 +42,8 @@ class HeadParams(ctypes.Structure):
                 ("magic", ctypes.c_uint32), ("shift", ctypes.c_int32),
                 ("use32", ctypes.c_int32), ("out_scale", ctypes.c_float),
                 ("s_q", ctypes.c_float), ("s_k", ctypes.c_float), ("s_v", ctypes.c_float),
-                ("unc32", ctypes.c_int32), ("magic9", ctypes.c_uint32)]
+                ("unc32", ctypes.c_int32), ("magic9", ctypes.c_uint32),
+                ("fratio", ctypes.c_float)]
 
 
 class AttnArgs(ctypes.Structure):

@@ -113,6 +113,7 @@ struct Cfg {
   }
   static constexpr int STAGE_PITCH = DP + 1;  // f32 epilogue staging row pitch (words, conflict-free)
   static_assert(OFF_TAB >= BM * STAGE_PITCH * 4, "epilogue staging must fit in Q/K/V stages");
+  static_assert(OFF_TAB % 512 == 0, "row-table base: idx * 512 is OR-ed into the address");
 };
 
 // Row tables: u32 [tab_entries][128] (conflict-free gathers) for nlut <= 64, else u8.
@@ -228,6 +229,10 @@ __device__ __forceinline__ void bwait(uint64_t* bar, uint32_t parity, bool spin)
 // pass-3 16-key group skip below the row's nonzero threshold (rows of >= 16 key tiles)
 #ifndef IA_GROUP_SKIP
 #define IA_GROUP_SKIP 1
+#endif
+// float form of the index map in passes 2-3 where it is exact (params.cuh float_idx_ok)
+#ifndef IA_FLOAT_IDX
+#define IA_FLOAT_IDX 1
 #endif
 #ifndef IA_PRODUCER_BACKOFF_NS
 #define IA_PRODUCER_BACKOFF_NS 0
@@ -949,6 +954,9 @@ __global__ void __launch_bounds__(Cfg<DP>::NTHREADS, 1)
     }
     if (dead) m = 0;
     const bool fast = hp.use32 != 0;
+    // the clipped distance delta = c_eff itself fits the 32-bit map (it need not when c_eff
+    // exceeds every reachable distance): cut-off chunks may then park excluded keys at lo
+    const bool fastc = fast && (2 * (int64_t)k + 1) * hp.c_eff < (int64_t(1) << 31);
     IdxMap im;
     im.init(m, hp, k);
     // Largest index any unmasked logit of this warp's rows can reach without the
@@ -962,6 +970,17 @@ __global__ void __launch_bounds__(Cfg<DP>::NTHREADS, 1)
     idx_hi = __reduce_max_sync(0xffffffffu, idx_hi);
     const bool uncl2 = hp.unc32 && idx_hi < 256u;                      // lut8 has 256 entries
     const bool uncl3 = hp.unc32 && wtab && idx_hi < (uint32_t)ntab;  // zero-extended row table
+    // Float (denormal) form of the index map (params.cuh float_idx_ok): valid for this
+    // warp's unclipped range (flu) / for clipped distances (flc).  The integer distance
+    // delta = m - a (< 2^23 for d <= 256), read as an f32 bit pattern, IS the denormal
+    // delta * 2^-149, so one FMA with a denormal addend A * 2^-149 leaves
+    // round(delta * r) + A in the result's bit pattern: a shared-memory address.
+    const float rf = hp.fratio;  // 0: c_eff too large for the float form
+    const bool flu = IA_FLOAT_IDX && rf != 0.0f && float_idx_ok(hp.c_eff, (int64_t)idx_hi);
+    const bool flc = IA_FLOAT_IDX && rf != 0.0f && float_idx_ok(hp.c_eff, (int64_t)k);
+    const float rf9 = rf * 512.0f;  // pass 3: idx * 512 + 9 fraction bits
+    const float lutden = __uint_as_float(smem_u32(lut8));  // pass 2 addend: &lut8[0]
+    const uint32_t mI = (uint32_t)m;
 
     // ---- pass 2: idx, e = lut[idx], S = sum e (softmax.py:144-155)
     uint32_t S = 0;
@@ -989,23 +1008,44 @@ __global__ void __launch_bounds__(Cfg<DP>::NTHREADS, 1)
         // masked keys (e >= cut) take idx = k, lut[k] = 0 (softmax.py:187-188); dead /
         // invalid rows (cut = 0) sum to S = 0 and get an all-zero table
         const int cut = (row_valid && !dead) ? lim - j0 + 1 : 0;
-        if (!p.mask_bits && fast) {
-          const bool any_cut = __any_sync(0xffffffffu, cut < 64);
-          if (uncl2 && !any_cut) {
+        const bool any_cut = __any_sync(0xffffffffu, cut < 64);
+        if (!p.mask_bits && fast && (!any_cut || fastc)) {
+          if (any_cut) {
+            // Cut-off chunk (diagonal / ragged tile): nothing to add if every key of every
+            // row is excluded; else excluded keys take the clip floor lo (delta = c_eff ->
+            // idx = k, lut[k] = 0) and the chunk runs the clipped fast path.
+            if (!__any_sync(0xffffffffu, cut > 0)) continue;
+            const uint32_t lo_u = (uint32_t)im.lo;
+#pragma unroll
+            for (int e = 0; e < 32; ++e) {
+              va[e] = e < cut ? va[e] : lo_u;
+              vb[e] = e + 32 < cut ? vb[e] : lo_u;
+            }
+          }
+          const bool unc = uncl2 && !any_cut;
+          if ((unc && flu) || flc) {
+            // RN(delta * r + &lut8) in denormal units: the bit pattern is &lut8[idx]
+            auto fsum = [&](auto clip) {
+              const int32_t lo = im.lo;
+#pragma unroll
+              for (int e = 0; e < 32; ++e) {
+                const uint32_t xa = decltype(clip)::value ? (uint32_t)max((int32_t)va[e], lo) : va[e];
+                const uint32_t xb = decltype(clip)::value ? (uint32_t)max((int32_t)vb[e], lo) : vb[e];
+                float fa, fb;
+                fma_rn_f32x2(fa, fb, __uint_as_float(mI - xa), __uint_as_float(mI - xb), rf, lutden);
+                S += lds_u8(__float_as_uint(fa)) + lds_u8(__float_as_uint(fb));
+              }
+            };
+            if (unc && flu) fsum(std::false_type{});
+            else fsum(std::true_type{});
+          } else if (unc) {
 #pragma unroll
             for (int e = 0; e < 32; ++e)
               S += (uint32_t)lut8[im.idx_u((int32_t)va[e])] + (uint32_t)lut8[im.idx_u((int32_t)vb[e])];
-          } else if (!any_cut) {
+          } else {
 #pragma unroll
             for (int e = 0; e < 32; ++e)
               S += (uint32_t)lut8[im.idx_s((int32_t)va[e])] + (uint32_t)lut8[im.idx_s((int32_t)vb[e])];
-          } else {
-#pragma unroll
-            for (int e = 0; e < 32; ++e) {
-              const uint32_t x0 = e < cut ? im.idx_s((int32_t)va[e]) : k;  // lut8[k] = 0
-              const uint32_t x1 = e + 32 < cut ? im.idx_s((int32_t)vb[e]) : k;
-              S += (uint32_t)lut8[x0] + (uint32_t)lut8[x1];
-            }
           }
         } else if (row_valid && !dead) {
           const uint32_t ma = chunk_mask(p, i, j0, lim), mbb = chunk_mask(p, i, j0 + 32, lim);
@@ -1110,6 +1150,7 @@ __global__ void __launch_bounds__(Cfg<DP>::NTHREADS, 1)
 #pragma unroll
         for (int q = 0; q < 16; ++q) pk[q] = 0u;
         const int cut = (row_valid && !dead) ? lim - j0 + 1 : 0;
+        const bool any_cut = __any_sync(0xffffffffu, cut < 64);
         if (SKEL) {
         } else if (QO) {
           // p^ = floor(exp(real - max) * (scale / sum) + 0.5) (pipeline.py:130-140, 281)
@@ -1128,9 +1169,66 @@ __global__ void __launch_bounds__(Cfg<DP>::NTHREADS, 1)
               pk[8 + (e >> 2)] |= bb << (8 * (e & 3));
             }
           }
-        } else if (!p.mask_bits && fast && wtab) {
-          const bool any_cut = __any_sync(0xffffffffu, cut < 64);
-          if (!any_cut && m9) {
+        } else if (!p.mask_bits && fast && wtab && (!any_cut || fastc)) {
+          bool live = true;  // some key of some row of the warp is not excluded
+          if (any_cut) {
+            // cut-off chunk: excluded keys take the clip floor lo (idx = k, table entry 0)
+            // and the chunk runs the clipped fast path; all excluded: P^ = 0
+            live = __any_sync(0xffffffffu, cut > 0);
+            if (live) {
+              const uint32_t lo_u = (uint32_t)im.lo;
+#pragma unroll
+              for (int e = 0; e < 32; ++e) {
+                va[e] = e < cut ? va[e] : lo_u;
+                vb[e] = e + 32 < cut ? vb[e] : lo_u;
+              }
+            }
+          }
+          const bool unc = uncl3 && !any_cut;
+          if (!live) {
+          } else if ((unc && flu) || flc) {
+            // RZ(delta * 512 r + tab0 + 256) in denormal units: tab0 + idx * 512 + 9 fraction
+            // bits; the row-table address is one LOP3 away (as with magic9)
+            // addend: (tab0 + 256) * 2^-149 (the 256 is the map's + 1/2 in units of 1/512)
+            const float tabden = __uint_as_float(tab0 + 256u);
+            const int32_t lo = im.lo;
+            auto fgroups = [&](auto clip, auto skip) {
+#pragma unroll
+              for (int g = 0; g < 4; ++g) {
+                const uint32_t* v16 = g < 2 ? &va[16 * g] : &vb[16 * (g - 2)];
+                if (decltype(skip)::value) {
+                  int32_t gm = (int32_t)v16[0];
+#pragma unroll
+                  for (int e = 1; e < 16; ++e) gm = max(gm, (int32_t)v16[e]);
+                  if (!__any_sync(0xffffffffu, gm >= theta)) continue;  // pk stays 0
+                }
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                  const uint32_t* v4 = v16 + 4 * q;
+                  uint32_t pw[4];
+#pragma unroll
+                  for (int e = 0; e < 4; e += 2) {
+                    const uint32_t x0 = decltype(clip)::value ? (uint32_t)max((int32_t)v4[e], lo) : v4[e];
+                    const uint32_t x1 = decltype(clip)::value ? (uint32_t)max((int32_t)v4[e + 1], lo) : v4[e + 1];
+                    float f0, f1;
+                    fma_rz_f32x2(f0, f1, __uint_as_float(mI - x0), __uint_as_float(mI - x1), rf9, tabden);
+                    pw[e] = lds_u32(and_or(__float_as_uint(f0), 0xFFFFFE00u, row4));
+                    pw[e + 1] = lds_u32(and_or(__float_as_uint(f1), 0xFFFFFE00u, row4));
+                  }
+                  pk[4 * g + q] = __byte_perm(__byte_perm(pw[0], pw[1], 0x0040),
+                                              __byte_perm(pw[2], pw[3], 0x0040), 0x5410);
+                }
+              }
+            };
+            const bool skip = IA_GROUP_SKIP && n_kt >= 16;
+            if (unc && flu) {
+              if (skip) fgroups(std::false_type{}, std::true_type{});
+              else fgroups(std::false_type{}, std::false_type{});
+            } else {
+              if (skip) fgroups(std::true_type{}, std::true_type{});
+              else fgroups(std::true_type{}, std::false_type{});
+            }
+          } else if (m9) {
             // address = tab0 + ((umulhi(n, magic9) & ~511) | row*4): IMAD, IMAD.HI, LOP3,
             // LDS per logit (+ the clip VIMNMX when the warp's index range exceeds the
             // table).  Groups of 16 keys below every row's threshold stay zero.
@@ -1164,14 +1262,14 @@ __global__ void __launch_bounds__(Cfg<DP>::NTHREADS, 1)
             // short rows (theta = INT_MIN) take the branch-free form: all 64 logits
             // interleave freely
             const bool skip = IA_GROUP_SKIP && n_kt >= 16;
-            if (uncl3) {
+            if (unc) {
               if (skip) groups(std::false_type{}, std::true_type{});
               else groups(std::false_type{}, std::false_type{});
             } else {
               if (skip) groups(std::true_type{}, std::true_type{});
               else groups(std::true_type{}, std::false_type{});
             }
-          } else if (!any_cut) {
+          } else {
 #pragma unroll
             for (int q = 0; q < 16; ++q) {
               const uint32_t* v4 = q < 8 ? &va[4 * q] : &vb[4 * (q - 8)];
@@ -1179,21 +1277,6 @@ __global__ void __launch_bounds__(Cfg<DP>::NTHREADS, 1)
               const uint32_t p1 = lds_u32(tab_row + (im.idx_s((int32_t)v4[1]) << 9));
               const uint32_t p2 = lds_u32(tab_row + (im.idx_s((int32_t)v4[2]) << 9));
               const uint32_t p3 = lds_u32(tab_row + (im.idx_s((int32_t)v4[3]) << 9));
-              pk[q] = __byte_perm(__byte_perm(p0, p1, 0x0040), __byte_perm(p2, p3, 0x0040), 0x5410);
-            }
-          } else {
-#pragma unroll
-            for (int q = 0; q < 16; ++q) {
-              const uint32_t* v4 = q < 8 ? &va[4 * q] : &vb[4 * (q - 8)];
-              const int eb = 4 * q;  // masked keys select table entry k (= 0)
-              const uint32_t x0 = eb + 0 < cut ? im.idx_s((int32_t)v4[0]) : k;
-              const uint32_t x1 = eb + 1 < cut ? im.idx_s((int32_t)v4[1]) : k;
-              const uint32_t x2 = eb + 2 < cut ? im.idx_s((int32_t)v4[2]) : k;
-              const uint32_t x3 = eb + 3 < cut ? im.idx_s((int32_t)v4[3]) : k;
-              const uint32_t p0 = lds_u32(tab_row + (x0 << 9));
-              const uint32_t p1 = lds_u32(tab_row + (x1 << 9));
-              const uint32_t p2 = lds_u32(tab_row + (x2 << 9));
-              const uint32_t p3 = lds_u32(tab_row + (x3 << 9));
               pk[q] = __byte_perm(__byte_perm(p0, p1, 0x0040), __byte_perm(p2, p3, 0x0040), 0x5410);
             }
           }

@@ -30,7 +30,7 @@ def test_library_loads_and_exports_every_declared_symbol():
     for name in declared:
         assert hasattr(L, name), f"{name} declared in include/intattn_b200.h but not exported"
     assert sorted(_lib.EXPORTS) == declared
-    assert L.ia_abi_version() == 4
+    assert L.ia_abi_version() == 5
 
 
 def test_status_strings():
