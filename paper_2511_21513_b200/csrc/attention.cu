@@ -234,6 +234,9 @@ __device__ __forceinline__ void bwait(uint64_t* bar, uint32_t parity, bool spin)
 #ifndef IA_FLOAT_IDX
 #define IA_FLOAT_IDX 1
 #endif
+#ifndef IA_SKIP_G
+#define IA_SKIP_G 8
+#endif
 #ifndef IA_PRODUCER_BACKOFF_NS
 #define IA_PRODUCER_BACKOFF_NS 0
 #endif
@@ -893,13 +896,17 @@ __global__ void __launch_bounds__(Cfg<DP>::NTHREADS, 1)
         } else if (XF(32)) {  // experiment: no pass-1 arithmetic
         } else if (!p.mask_bits) {
           if (!__any_sync(0xffffffffu, cut < 64)) {
+            // two 3-input VIMNMX3 chains per direction: one instruction per two logits
+            int32_t mx1 = mx, mn1 = mn;
 #pragma unroll
             for (int e = 0; e < 32; e += 2) {
-              mx = max(mx, max(max((int32_t)va[e], (int32_t)va[e + 1]),
-                               max((int32_t)vb[e], (int32_t)vb[e + 1])));
-              mn = min(mn, min(min((int32_t)va[e], (int32_t)va[e + 1]),
-                               min((int32_t)vb[e], (int32_t)vb[e + 1])));
+              mx = __vimax3_s32(mx, (int32_t)va[e], (int32_t)va[e + 1]);
+              mx1 = __vimax3_s32(mx1, (int32_t)vb[e], (int32_t)vb[e + 1]);
+              mn = __vimin3_s32(mn, (int32_t)va[e], (int32_t)va[e + 1]);
+              mn1 = __vimin3_s32(mn1, (int32_t)vb[e], (int32_t)vb[e + 1]);
             }
+            mx = max(mx, mx1);
+            mn = min(mn, mn1);
           } else {
 #pragma unroll
             for (int e = 0; e < 32; ++e) {
@@ -1193,18 +1200,19 @@ __global__ void __launch_bounds__(Cfg<DP>::NTHREADS, 1)
             const float tabden = __uint_as_float(tab0 + 256u);
             const int32_t lo = im.lo;
             auto fgroups = [&](auto clip, auto skip) {
+              constexpr int G = IA_SKIP_G;  // keys per skip group
 #pragma unroll
-              for (int g = 0; g < 4; ++g) {
-                const uint32_t* v16 = g < 2 ? &va[16 * g] : &vb[16 * (g - 2)];
+              for (int g = 0; g < 64 / G; ++g) {
+                const uint32_t* vg = g < 32 / G ? &va[G * g] : &vb[G * (g - 32 / G)];
                 if (decltype(skip)::value) {
-                  int32_t gm = (int32_t)v16[0];
+                  int32_t gm = (int32_t)vg[0];
 #pragma unroll
-                  for (int e = 1; e < 16; ++e) gm = max(gm, (int32_t)v16[e]);
+                  for (int e = 1; e < G; ++e) gm = max(gm, (int32_t)vg[e]);
                   if (!__any_sync(0xffffffffu, gm >= theta)) continue;  // pk stays 0
                 }
 #pragma unroll
-                for (int q = 0; q < 4; ++q) {
-                  const uint32_t* v4 = v16 + 4 * q;
+                for (int q = 0; q < G / 4; ++q) {
+                  const uint32_t* v4 = vg + 4 * q;
                   uint32_t pw[4];
 #pragma unroll
                   for (int e = 0; e < 4; e += 2) {
@@ -1215,8 +1223,8 @@ __global__ void __launch_bounds__(Cfg<DP>::NTHREADS, 1)
                     pw[e] = lds_u32(and_or(__float_as_uint(f0), 0xFFFFFE00u, row4));
                     pw[e + 1] = lds_u32(and_or(__float_as_uint(f1), 0xFFFFFE00u, row4));
                   }
-                  pk[4 * g + q] = __byte_perm(__byte_perm(pw[0], pw[1], 0x0040),
-                                              __byte_perm(pw[2], pw[3], 0x0040), 0x5410);
+                  pk[(G / 4) * g + q] = __byte_perm(__byte_perm(pw[0], pw[1], 0x0040),
+                                                    __byte_perm(pw[2], pw[3], 0x0040), 0x5410);
                 }
               }
             };
