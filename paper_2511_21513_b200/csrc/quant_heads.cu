@@ -7,7 +7,7 @@
 //   pass A: max |x| over the slab's valid rows (HBM read), folded into the slab's
 //           amax slot; the team meets at a per-slab arrival counter;
 //   pass B: s = max(amax, 1e-12f) / 127f and the quantise pass, re-reading the slab
-//           from L2 (teams x slab bytes is kept ~64 MB, under the 126 MB L2).
+//           from L2 (teams x slab bytes is kept ~96 MB, under the 126 MB L2, with L2 eviction hints).
 // Q^ / K^ are written row-major [L, d_pad] and V^ as the per-head transpose
 // [d_pad, l_pad] the fused kernel's P.V operand wants; padding rows / columns are 0.
 // Arithmetic is the same IEEE f32 sequence as quantize.cu (bit-identical results).
@@ -25,23 +25,78 @@ __device__ __forceinline__ float qh_scale(uint32_t amax_bits) {
 }
 // q = clip(round_half_away(x / s), +-127) with the quotient numpy computes (IEEE f32
 // x / s, quantize.py:121).  t = x * (1/s) is within |t| 2^-23 <= 2^-16 of it (|t| <= 127
-// + an ulp); unless |t| is within 2^-15 of a rounding boundary k + 0.5 (where the exact
-// quotient is taken), both round to the same integer, and the f32 sum |t| + 0.5 stays
-// 2^-16 away from an integer, so the rounded result is the reference's bit for bit.
-__device__ __forceinline__ uint32_t qh_q(float x, float s, float rcp) {
-  float t = __fmul_rn(x, rcp);
-  const float at = fabsf(t);
-  if (fabsf(__fsub_rn(__fsub_rn(at, floorf(at)), 0.5f)) <= 3.0517578125e-05f) t = __fdiv_rn(x, s);
+// + an ulp).  y = |t| + 0.5 (the reference's own f32 add, rounding.py:21) is floored by
+// one round-toward-zero add of 2^23 -- z = 2^23 + floor(y), the integer sits in z's
+// mantissa -- so no FRND / F2I conversion (quarter-rate pipe) is needed; y - floor(y) is
+// exact.  Unless that fraction is within 2^-14 of 0 or 1 (|t| near a rounding boundary
+// k + 0.5, where the exact quotient is taken instead), the exact quotient's y' lies
+// within 2^-15 of y on the same side of every integer, so floor(y') = floor(y): the
+// reference's result bit for bit.
+__device__ __forceinline__ float qh_add_rz(float a, float b) {
+  float r;
+  asm("add.rz.f32 %0, %1, %2;" : "=f"(r) : "f"(a), "f"(b));
+  return r;
+}
+// Fast form; `bad` is raised when the element sits within 2^-14 of a rounding boundary
+// and must be redone with the exact quotient (qh_q_exact) -- callers test it once per
+// 16 elements, so the common path is branch-free.
+__device__ __forceinline__ uint32_t qh_q_fast(float x, float rcp, bool& bad) {
+  const float t = __fmul_rn(x, rcp);
+  const float y = fminf(__fadd_rn(fabsf(t), 0.5f), 127.5f);  // rounding.py:21; quantize.py:122
+  const float z = qh_add_rz(y, 8388608.0f);
+  const float fr = __fsub_rn(y, __fsub_rn(z, 8388608.0f));
+  bad |= !(fr > 6.103515625e-05f && fr < 0.99993896484375f);
+  const uint32_t v = __float_as_uint(z) & 0xffu;  // floor(y) <= 127
+  return (t < 0.0f ? 0u - v : v) & 0xffu;
+}
+// The reference's own sequence on the exact quotient (rare path).
+__device__ __noinline__ uint32_t qh_q_exact(float x, float s) {
+  const float t = __fdiv_rn(x, s);
   float r = floorf(__fadd_rn(fabsf(t), 0.5f));   // rounding.py:21
   r = fminf(r, 127.0f);                          // quantize.py:122
   const int v = (int)r;
   return (uint32_t)(uint8_t)(int8_t)(t < 0.0f ? -v : v);
 }
+__device__ __forceinline__ uint32_t qh_pack4_fast(float4 v, float rcp, bool& bad) {
+  return qh_q_fast(v.x, rcp, bad) | (qh_q_fast(v.y, rcp, bad) << 8) |
+         (qh_q_fast(v.z, rcp, bad) << 16) | (qh_q_fast(v.w, rcp, bad) << 24);
+}
+__device__ __forceinline__ uint32_t qh_pack4_exact(float4 v, float s) {
+  return qh_q_exact(v.x, s) | (qh_q_exact(v.y, s) << 8) | (qh_q_exact(v.z, s) << 16) |
+         (qh_q_exact(v.w, s) << 24);
+}
 __device__ __forceinline__ uint32_t qh_pack4(float4 v, float s, float rcp) {
-  return qh_q(v.x, s, rcp) | (qh_q(v.y, s, rcp) << 8) | (qh_q(v.z, s, rcp) << 16) |
-         (qh_q(v.w, s, rcp) << 24);
+  bool bad = false;
+  const uint32_t w = qh_pack4_fast(v, rcp, bad);
+  return bad ? qh_pack4_exact(v, s) : w;
 }
 __device__ __forceinline__ uint32_t qh_abs(float x) { return __float_as_uint(x) & 0x7fffffffu; }
+
+// L2 eviction hints: the amax pass asks L2 to keep the slab (evict_last) for the quantise
+// pass, which reads it with evict_first (done with it) and writes its int8 output as
+// streaming data, so neither the pass-B reads nor the outputs push later slabs out.
+__device__ __forceinline__ uint64_t l2_policy_evict_last() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ uint64_t l2_policy_evict_first() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ float4 ldg_hint(const float4* ptr, uint64_t pol) {
+  float4 v;
+  asm volatile("ld.global.nc.L2::cache_hint.v4.f32 {%0, %1, %2, %3}, [%4], %5;"
+               : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+               : "l"(ptr), "l"(pol));
+  return v;
+}
+__device__ __forceinline__ void stg_hint(void* ptr, uint4 v, uint64_t pol) {
+  asm volatile("st.global.L2::cache_hint.v4.b32 [%0], {%1, %2, %3, %4}, %5;" ::"l"(ptr), "r"(v.x),
+               "r"(v.y), "r"(v.z), "r"(v.w), "l"(pol)
+               : "memory");
+}
 
 struct QHArgs {
   const float* x[3];
@@ -60,7 +115,7 @@ struct QHArgs {
   int kb;    // V^T block: keys per block (multiple of 16, kb/4 * d_pad/4 <= QH_THREADS)
   int mode;  // 0: fused (team barrier), 1: amax only, 2: quantise only (slabs in reverse order)
   int per_tensor;  // split modes only: one amax / scale slot per tensor (ti), not per slab
-  int pf;    // mode 0: bulk-prefetch the team's next slab into L2 before the team barrier
+  int hints;  // mode 0 L2 eviction hints: 1 pass A evict_last, 2 pass B evict_first, 4 stores evict_first
 };
 
 constexpr int QH_THREADS = 512;
@@ -71,71 +126,67 @@ __global__ void __launch_bounds__(QH_THREADS, 3) quant_heads_kernel(const QHArgs
   extern __shared__ __align__(16) uint8_t tile[];  // [d_pad][kb + 4] bytes (V^T blocks)
   const int T = a.team;
   const int team = blockIdx.x / T, rank = blockIdx.x - (blockIdx.x / T) * T;
-  // split modes: one slab per team, no barrier; the quantise pass walks the slabs in the
-  // reverse of the amax pass's order so its first reads hit the slabs still in L2
   // Teams stride over the slabs (split modes with n_teams == n_slabs: one slab each).
+  // Split modes: no barrier; the quantise pass walks the slabs in the reverse of the amax
+  // pass's order so its first reads hit the slabs still in L2.
   const int64_t s_step = a.n_teams;
   const int tid = threadIdx.x;
   const int64_t L = a.L, d = a.d;
   const int64_t d4 = d >> 2;
-  for (int64_t j = team; j < a.n_slabs; j += s_step) {
-    const int64_t s = a.mode == 2 ? a.n_slabs - 1 - j : j;
-    int ti = 0;
-    int64_t g = s;
-    while (ti < 2 && g >= a.ngroups[ti]) { g -= a.ngroups[ti]; ++ti; }
-    int64_t nvalid = L;
+  const uint64_t pol_keep = l2_policy_evict_last(), pol_drop = l2_policy_evict_first();
+  const bool hint_a = a.mode == 0 && (a.hints & 1), hint_b = a.mode == 0 && (a.hints & 2);
+  const bool hint_st = a.mode == 0 && (a.hints & 4);
+
+  struct Slab {
+    int ti;
+    int64_t g, nvalid, slot;
+    const float4* base;
+  };
+  auto slab_of = [&](int64_t s) {
+    Slab sl;
+    sl.ti = 0;
+    sl.g = s;
+    while (sl.ti < 2 && sl.g >= a.ngroups[sl.ti]) { sl.g -= a.ngroups[sl.ti]; ++sl.ti; }
+    sl.nvalid = L;
     if (a.valid_rows) {
-      const int64_t v = a.valid_rows[g / a.valid_div[ti]];
-      nvalid = v < 0 ? 0 : (v < L ? v : L);
+      const int64_t v = a.valid_rows[sl.g / a.valid_div[sl.ti]];
+      sl.nvalid = v < 0 ? 0 : (v < L ? v : L);
     }
-    const float4* base = reinterpret_cast<const float4*>(a.x[ti] + g * L * d);
-    // ---- pass A: max |x| over the valid rows (quantize.py:92-101)
-    const int64_t n4 = a.mode == 2 ? 0 : nvalid * d4;
+    sl.base = reinterpret_cast<const float4*>(a.x[sl.ti] + sl.g * L * d);
+    sl.slot = a.per_tensor ? sl.ti : s;
+    return sl;
+  };
+
+  // ---- pass A: max |x| over the valid rows (quantize.py:92-101), folded into the slab's
+  // amax slot; mode 0: this CTA then arrives at the slab's counter
+  auto pass_a = [&](int64_t s) {
+    const Slab sl = slab_of(s);
+    const float4* base = sl.base;
+    const int64_t n4 = sl.nvalid * d4;
     uint32_t m = 0;
-    {
-      // four independent 16-byte loads in flight per thread (HBM needs the MLP)
-      const int64_t step = (int64_t)T * QH_THREADS;
-      int64_t i = (int64_t)rank * QH_THREADS + tid;
+    auto fold = [&](const float4& v) {
+      m = max(m, max(max(qh_abs(v.x), qh_abs(v.y)), max(qh_abs(v.z), qh_abs(v.w))));
+    };
+    // four independent 16-byte loads in flight per thread (HBM needs the MLP)
+    const int64_t step = (int64_t)T * QH_THREADS;
+    int64_t i = (int64_t)rank * QH_THREADS + tid;
+    if (hint_a) {
+      for (; i + 3 * step < n4; i += 4 * step) {
+        const float4 v0 = ldg_hint(base + i, pol_keep), v1 = ldg_hint(base + i + step, pol_keep);
+        const float4 v2 = ldg_hint(base + i + 2 * step, pol_keep), v3 = ldg_hint(base + i + 3 * step, pol_keep);
+        fold(v0); fold(v1); fold(v2); fold(v3);
+      }
+      for (; i < n4; i += step) fold(ldg_hint(base + i, pol_keep));
+    } else {
       for (; i + 3 * step < n4; i += 4 * step) {
         const float4 v0 = __ldg(base + i), v1 = __ldg(base + i + step);
         const float4 v2 = __ldg(base + i + 2 * step), v3 = __ldg(base + i + 3 * step);
-        m = max(m, max(max(qh_abs(v0.x), qh_abs(v0.y)), max(qh_abs(v0.z), qh_abs(v0.w))));
-        m = max(m, max(max(qh_abs(v1.x), qh_abs(v1.y)), max(qh_abs(v1.z), qh_abs(v1.w))));
-        m = max(m, max(max(qh_abs(v2.x), qh_abs(v2.y)), max(qh_abs(v2.z), qh_abs(v2.w))));
-        m = max(m, max(max(qh_abs(v3.x), qh_abs(v3.y)), max(qh_abs(v3.z), qh_abs(v3.w))));
+        fold(v0); fold(v1); fold(v2); fold(v3);
       }
-      for (; i < n4; i += step) {
-        const float4 v = __ldg(base + i);
-        m = max(m, max(max(qh_abs(v.x), qh_abs(v.y)), max(qh_abs(v.z), qh_abs(v.w))));
-      }
+      for (; i < n4; i += step) fold(__ldg(base + i));
     }
-    if (a.pf && a.mode == 0 && tid == 0 && s + s_step < a.n_slabs) {
-      // The next slab streams into L2 while this one waits at the barrier and runs
-      // pass B, so HBM stays busy across the team's serialising steps.  Each CTA of
-      // the team prefetches one contiguous 1/T of the next slab's valid rows.
-      const int64_t s2 = s + s_step;
-      int t2 = 0;
-      int64_t g2 = s2;
-      while (t2 < 2 && g2 >= a.ngroups[t2]) { g2 -= a.ngroups[t2]; ++t2; }
-      int64_t nv2 = L;
-      if (a.valid_rows) {
-        const int64_t v = a.valid_rows[g2 / a.valid_div[t2]];
-        nv2 = v < 0 ? 0 : (v < L ? v : L);
-      }
-      const int64_t bytes = nv2 * d * 4;
-      const int64_t per = ((bytes + T - 1) / T + 15) & ~(int64_t)15;
-      int64_t lo = (int64_t)rank * per, hi = lo + per;
-      hi = hi < bytes ? hi : bytes;
-      const char* p2 = reinterpret_cast<const char*>(a.x[t2] + g2 * L * d);
-      for (; lo < hi; lo += 32768) {
-        const int64_t n = (hi - lo < 32768 ? hi - lo : 32768) & ~(int64_t)15;
-        if (n > 0)
-          asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p2 + lo), "r"((uint32_t)n)
-                       : "memory");
-      }
-    }
-    const int64_t slot = a.per_tensor ? ti : s;
     m = warp_max_u32(m);
+    __syncthreads();  // red[] may still be read by the previous reduction's warp 0
     if ((tid & 31) == 0) red[tid >> 5] = m;
     __syncthreads();
     if (tid < 32) {
@@ -143,60 +194,77 @@ __global__ void __launch_bounds__(QH_THREADS, 3) quant_heads_kernel(const QHArgs
       m = warp_max_u32(m);
       if (tid == 0) {
         // NaN bit patterns sort above +inf: a non-finite element lifts m >= 0x7f800000
-        if (a.mode != 2) {
-          if (m >= 0x7f800000u) atomicOr(reinterpret_cast<unsigned int*>(a.err), 1u);
-          else if (m) atomicMax(a.amax + slot, m);
-        }
+        if (m >= 0x7f800000u) atomicOr(reinterpret_cast<unsigned int*>(a.err), 1u);
+        else if (m) atomicMax(a.amax + sl.slot, m);
         if (a.mode == 0) {
           __threadfence();
           atomicAdd(a.count + s, 1);
-          // The team meets here.  Mode 0 is only ever launched cooperatively
-          // (cudaLaunchAttributeCooperative), so every CTA of the grid is co-resident and
-          // the wait ends; the bound is a second line of defence: after ~2^26 polls
-          // (seconds) the kernel flags IA_QH_ERR_BARRIER and carries on, so the call
-          // fails loudly instead of hanging.
-          uint32_t polls = 0;
-          while (*reinterpret_cast<volatile int32_t*>(a.count + s) < T) {
-            __nanosleep(128);
-            if (++polls == (1u << 26)) {
-              atomicOr(reinterpret_cast<unsigned int*>(a.err), 2u);
-              break;
-            }
-          }
-          __threadfence();
-        }
-        if (a.mode != 1) {
-          const float sc = qh_scale(*reinterpret_cast<volatile uint32_t*>(a.amax + slot));
-          s_sh = sc;
-          if (rank == 0) a.scales[slot] = sc;  // per tensor: every slab stores the same value
         }
       }
     }
+  };
+
+  // ---- pass B: the team's amax is final (mode 0: once every CTA of the team has arrived);
+  // s = max(amax, 1e-12f) / 127f and the quantise pass (mode 0: slab re-read from L2)
+  auto pass_b = [&](int64_t s) {
+    const Slab sl = slab_of(s);
+    const float4* base = sl.base;
+    const int64_t nvalid = sl.nvalid, g = sl.g;
+    const int ti = sl.ti;
+    if (tid == 0) {
+      if (a.mode == 0) {
+        // Mode 0 is only ever launched cooperatively (cudaLaunchAttributeCooperative), so
+        // every CTA of the grid is co-resident and the wait ends.  The bound is a second
+        // line of defence: after ~2^26 polls (seconds) the kernel flags
+        // IA_QH_ERR_BARRIER and carries on, so the call fails loudly instead of hanging.
+        uint32_t polls = 0;
+        while (*reinterpret_cast<volatile int32_t*>(a.count + s) < T) {
+          __nanosleep(128);
+          if (++polls == (1u << 26)) {
+            atomicOr(reinterpret_cast<unsigned int*>(a.err), 2u);
+            break;
+          }
+        }
+        __threadfence();
+      }
+      const float sc0 = qh_scale(*reinterpret_cast<volatile uint32_t*>(a.amax + sl.slot));
+      s_sh = sc0;
+      if (rank == 0) a.scales[sl.slot] = sc0;  // per tensor: every slab stores the same value
+    }
     __syncthreads();
-    if (a.mode == 1) continue;  // amax only
     const float sc = s_sh;
     const float rc = __frcp_rn(sc);
-    // ---- pass B: quantise (slab re-read from L2)
+    auto ld = [&](const float4* ptr) { return hint_b ? ldg_hint(ptr, pol_drop) : __ldg(ptr); };
+    auto st = [&](void* ptr, uint4 v) {
+      if (hint_st) stg_hint(ptr, v, pol_drop);
+      else *reinterpret_cast<uint4*>(ptr) = v;
+    };
     if (!a.transpose[ti]) {
       const int cpr = (int)(a.d_pad >> 4);  // 16-byte output chunks per row
       int8_t* og = a.out[ti] + g * L * a.d_pad;
       const int64_t nch = L * cpr;
+      const int lg = (cpr & (cpr - 1)) == 0 ? __ffs(cpr) - 1 : -1;  // power-of-two row pitch: shifts
       for (int64_t j = (int64_t)rank * QH_THREADS + tid; j < nch; j += (int64_t)T * QH_THREADS) {
-        const int64_t r = j / cpr;
+        const int64_t r = lg >= 0 ? (j >> lg) : j / cpr;
         const int c0 = (int)(j - r * cpr) << 4;
         uint4 o = make_uint4(0u, 0u, 0u, 0u);
         if (r < nvalid && c0 < d) {
           const float4* xr = base + r * d4 + (c0 >> 2);
           if (c0 + 16 <= d) {
-            const float4 v0 = __ldg(xr), v1 = __ldg(xr + 1), v2 = __ldg(xr + 2), v3 = __ldg(xr + 3);
-            o = make_uint4(qh_pack4(v0, sc, rc), qh_pack4(v1, sc, rc), qh_pack4(v2, sc, rc), qh_pack4(v3, sc, rc));
+            const float4 v0 = ld(xr), v1 = ld(xr + 1), v2 = ld(xr + 2), v3 = ld(xr + 3);
+            bool bad = false;
+            o = make_uint4(qh_pack4_fast(v0, rc, bad), qh_pack4_fast(v1, rc, bad),
+                           qh_pack4_fast(v2, rc, bad), qh_pack4_fast(v3, rc, bad));
+            if (bad)
+              o = make_uint4(qh_pack4_exact(v0, sc), qh_pack4_exact(v1, sc), qh_pack4_exact(v2, sc),
+                             qh_pack4_exact(v3, sc));
           } else {
             uint32_t w[4] = {0u, 0u, 0u, 0u};
-            for (int e = 0; e < 4 && c0 + 4 * e < d; ++e) w[e] = qh_pack4(__ldg(xr + e), sc, rc);
+            for (int e = 0; e < 4 && c0 + 4 * e < d; ++e) w[e] = qh_pack4(ld(xr + e), sc, rc);
             o = make_uint4(w[0], w[1], w[2], w[3]);
           }
         }
-        *reinterpret_cast<uint4*>(og + r * a.d_pad + c0) = o;
+        st(og + r * a.d_pad + c0, o);
       }
     } else {
       // V^T: blocks of kb keys.  Each thread loads a 4-key x 4-column patch (four
@@ -217,11 +285,16 @@ __global__ void __launch_bounds__(QH_THREADS, 3) quant_heads_kernel(const QHArgs
           float4 x4[4];
 #pragma unroll
           for (int i = 0; i < 4; ++i)
-            x4[i] = (rr + i < nvalid && c4 < d) ? __ldg(base + (rr + i) * d4 + (c4 >> 2))
+            x4[i] = (rr + i < nvalid && c4 < d) ? ld(base + (rr + i) * d4 + (c4 >> 2))
                                                 : make_float4(0.f, 0.f, 0.f, 0.f);
           uint32_t w[4];
+          bool bad = false;
 #pragma unroll
-          for (int i = 0; i < 4; ++i) w[i] = (rr + i < nvalid && c4 < d) ? qh_pack4(x4[i], sc, rc) : 0u;
+          for (int i = 0; i < 4; ++i) w[i] = qh_pack4_fast(x4[i], rc, bad);  // padding: x = 0 -> 0
+          if (bad) {
+#pragma unroll
+            for (int i = 0; i < 4; ++i) w[i] = qh_pack4_exact(x4[i], sc);
+          }
           const uint32_t lo01 = __byte_perm(w[0], w[1], 0x5140), hi01 = __byte_perm(w[0], w[1], 0x7362);
           const uint32_t lo23 = __byte_perm(w[2], w[3], 0x5140), hi23 = __byte_perm(w[2], w[3], 0x7362);
           tw[(c4 + 0) * pw + rg] = __byte_perm(lo01, lo23, 0x5410);
@@ -236,13 +309,24 @@ __global__ void __launch_bounds__(QH_THREADS, 3) quant_heads_kernel(const QHArgs
           const int64_t r = r0 + 16 * u;
           if (r < a.l_pad) {
             const uint32_t* src = tw + c * pw + 4 * u;
-            *reinterpret_cast<uint4*>(og + (int64_t)c * a.l_pad + r) = make_uint4(src[0], src[1], src[2], src[3]);
+            st(og + (int64_t)c * a.l_pad + r, make_uint4(src[0], src[1], src[2], src[3]));
           }
         }
         __syncthreads();
       }
     }
-    __syncthreads();
+    __syncthreads();  // s_sh is rewritten by the next slab's thread 0
+  };
+
+  if (a.mode == 1) {
+    for (int64_t j = team; j < a.n_slabs; j += s_step) pass_a(j);
+  } else if (a.mode == 2) {
+    for (int64_t j = team; j < a.n_slabs; j += s_step) pass_b(a.n_slabs - 1 - j);
+  } else {
+    for (int64_t j = team; j < a.n_slabs; j += s_step) {
+      pass_a(j);
+      pass_b(j);
+    }
   }
 }
 
@@ -319,9 +403,13 @@ static int quant_heads_launch(const float* q, const float* k, const float* v, in
   const int64_t slab_bytes = L * d * 4;
   const int64_t slab_elems = L * d;
   // IA_QH_L2MB / IA_QH_TEAM override the L2 budget and team size (A/B runs only)
-  static const int l2mb_env = dev_knob("IA_QH_L2MB", 64);
+  static const int l2mb_env = dev_knob("IA_QH_L2MB", 96);
   static const int team_env = dev_knob("IA_QH_TEAM", 0);
-  int64_t target = ((int64_t)l2mb_env << 20) / (slab_bytes > 0 ? slab_bytes : 1);  // slabs in flight (~64 MB)
+  static const int hints_env = dev_knob("IA_QH_HINTS", 7);
+  a.hints = hints_env;
+  // teams = slabs in flight in L2 (~96 MB: measured best of 32..800 on C4 / C5; smaller
+  // teams pay less at each barrier, and the evict_last / evict_first hints keep the re-read hits)
+  int64_t target = ((int64_t)l2mb_env << 20) / (slab_bytes > 0 ? slab_bytes : 1);
   target = target < 1 ? 1 : (target > a.n_slabs ? a.n_slabs : target);
   int64_t team = grid_max / target;
   const int64_t want = (slab_elems + QH_THREADS * 16 - 1) / (QH_THREADS * 16);  // >= 16 elem/thread
@@ -334,8 +422,6 @@ static int quant_heads_launch(const float* q, const float* k, const float* v, in
   a.team = (int)team;
   a.mode = 0;
   a.per_tensor = per_tensor;
-  static const int pf_env = dev_knob("IA_QH_PF", 0);
-  a.pf = pf_env;
   // Many small slabs (C3: 96 x 1 MB) spend more on team barriers than on bytes: run the
   // amax and quantise passes as two barrier-free launches instead (IA_QH_SPLIT=0/1
   // forces either form, for A/B checks).
