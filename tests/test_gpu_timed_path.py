@@ -90,3 +90,42 @@ def test_attention_graph_replay_bit_exact_and_live_inputs():
     g.replay()
     want, _ = O.attention_batched(q.cpu().numpy(), k.cpu().numpy(), v.cpu().numpy(), causal=True)
     assert np.array_equal(out.cpu().numpy().view(np.uint32), want.view(np.uint32))
+
+
+def _fused_ms(wl, softmax, iters=15):
+    """Median device time of the fused kernel stage (quantised -> attention) of the timed form."""
+    import statistics
+
+    class T:
+        def __init__(self):
+            self.ev = {}
+
+        def mark(self, n):
+            e = torch.cuda.Event(enable_timing=True)
+            e.record()
+            self.ev[n] = e
+
+    dev = torch.device("cuda", 0)
+    q, k, v = (torch.from_numpy(x).to(dev) for x in (wl.q, wl.k, wl.v))
+    out = torch.empty_like(q)
+    kw = dict(causal=wl.causal, scale_granularity=wl.scale_granularity, lut=E.lut_bytes(5, 6.6),
+              out=out, check_finite=False, softmax=softmax)
+    for _ in range(3):
+        E.attention(q, k, v, **kw)
+    ts = []
+    for _ in range(iters):
+        t = T()
+        E.attention(q, k, v, timer=t, **kw)
+        ts.append(t)
+    torch.cuda.synchronize()
+    return statistics.median(t.ev["quantized"].elapsed_time(t.ev["attention"]) for t in ts)
+
+
+def test_breakdown_consistency_index_beats_quant_only_at_l2048():
+    """The B200 analogue of the reference's 'breakdown consistency' acceptance (SPEC.md:337,
+    :469): from L = 2048 on, IndexSoftmax attention must not be slower than the quant-only
+    comparator (same quantiser, same MMAs, f32 exp softmax).  C3 is the L = 2048 config."""
+    wl = workloads.make("C3")
+    idx = _fused_ms(wl, "index")
+    flt = _fused_ms(wl, "float")
+    assert idx < flt, f"IndexSoftmax {idx:.4f} ms vs quant-only {flt:.4f} ms on C3"
