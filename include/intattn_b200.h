@@ -123,8 +123,8 @@ typedef struct ia_head_params {
   float s_q, s_k, s_v;
   int32_t unc32;    /* 1: the magic is also exact without the clip (n up to 2k*2*d*127^2 + c_eff) */
   uint32_t magic9;  /* 0, or: idx * 512 = umulhi(n, magic9) & ~511 for the clipped n range */
-  float fratio;     /* 0, or the smallest f32 above k / c_eff (c_eff < 2^23): the float form
-                     * idx = RN(delta * fratio) is exact while c_eff (2 idx_max + 1) < 2^23 */
+  float fratio;     /* 0, or the largest f32 below k / c_eff when c_eff (2k + 1) < 2^23: the float
+                     * form idx = k - RN(max(a - (m - c_eff), 0) * fratio) is then exact */
 } ia_head_params;
 
 int ia_head_params_host(double c, int64_t d, int nlut, int p_scale, float s_q, float s_k,

@@ -498,6 +498,7 @@ __global__ void __launch_bounds__(Cfg<DP>::NTHREADS, 1)
   constexpr int NWG = C::NWG;
   extern __shared__ uint8_t smem_raw[];
   __shared__ uint8_t lut8[256];  // static: LDS.U8 [idx + const] in the pass-2 gather
+  __shared__ uint8_t lut8r[256];  // reversed: lut8r[j] = lut[k - j] (float form, j = k - idx)
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~uintptr_t(1023));
   const int nlut = p.nlut;
@@ -576,7 +577,10 @@ __global__ void __launch_bounds__(Cfg<DP>::NTHREADS, 1)
     tmem_alloc(tmem_slot, TMEM_COLS);
     tmem_relinquish();
   }
-  for (int t = threadIdx.x; t < 256; t += C::NTHREADS) lut8[t] = t < nlut ? p.lut[t] : 0;
+  for (int t = threadIdx.x; t < 256; t += C::NTHREADS) {
+    lut8[t] = t < nlut ? p.lut[t] : 0;
+    lut8r[t] = t < nlut ? p.lut[nlut - 1 - t] : 0;
+  }
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
@@ -829,8 +833,13 @@ __global__ void __launch_bounds__(Cfg<DP>::NTHREADS, 1)
                            p_full, p_free, s_base, wg, row, lane, i, lim, bh, n_kt, row_valid,
                            resident, s_ph);
     } else {
-    // ---- pass 1: row max over unmasked keys (softmax.py:139-143, :174-179); the row
-    // min rides along (free: pass 1 waits on the MMA) to size the unclipped index range
+    // Float (denormal) form of the index map (params.cuh): one path for every row, clip
+    // included, so pass 1 needs the row max only.
+    const float rf = hp.fratio;  // 0: c_eff too large for the float form
+    // (needs the u32 row tables and cut-off masks only: dense masks take the generic path)
+    const bool flc = IA_FLOAT_IDX && rf != 0.0f && wtab && !p.mask_bits;
+    // ---- pass 1: row max over unmasked keys (softmax.py:139-143, :174-179); for the
+    // integer map the row min rides along to size the unclipped index range
     int32_t mx = INT_MIN, mn = INT_MAX;
     // QO: running max (real units) and sum of exp(real - qm); real = f32(a) * alpha in f32
     // as the reference (pipeline.py:277-279); f32(a) * alpha is monotone in a, so the
@@ -898,12 +907,20 @@ __global__ void __launch_bounds__(Cfg<DP>::NTHREADS, 1)
           if (!__any_sync(0xffffffffu, cut < 64)) {
             // two 3-input VIMNMX3 chains per direction: one instruction per two logits
             int32_t mx1 = mx, mn1 = mn;
+            if (flc) {
 #pragma unroll
-            for (int e = 0; e < 32; e += 2) {
-              mx = __vimax3_s32(mx, (int32_t)va[e], (int32_t)va[e + 1]);
-              mx1 = __vimax3_s32(mx1, (int32_t)vb[e], (int32_t)vb[e + 1]);
-              mn = __vimin3_s32(mn, (int32_t)va[e], (int32_t)va[e + 1]);
-              mn1 = __vimin3_s32(mn1, (int32_t)vb[e], (int32_t)vb[e + 1]);
+              for (int e = 0; e < 32; e += 2) {
+                mx = __vimax3_s32(mx, (int32_t)va[e], (int32_t)va[e + 1]);
+                mx1 = __vimax3_s32(mx1, (int32_t)vb[e], (int32_t)vb[e + 1]);
+              }
+            } else {
+#pragma unroll
+              for (int e = 0; e < 32; e += 2) {
+                mx = __vimax3_s32(mx, (int32_t)va[e], (int32_t)va[e + 1]);
+                mx1 = __vimax3_s32(mx1, (int32_t)vb[e], (int32_t)vb[e + 1]);
+                mn = __vimin3_s32(mn, (int32_t)va[e], (int32_t)va[e + 1]);
+                mn1 = __vimin3_s32(mn1, (int32_t)vb[e], (int32_t)vb[e + 1]);
+              }
             }
             mx = max(mx, mx1);
             mn = min(mn, mn1);
@@ -975,19 +992,15 @@ __global__ void __launch_bounds__(Cfg<DP>::NTHREADS, 1)
       idx_hi = hi > 0x7fffffff ? 0x7fffffffu : (uint32_t)hi;
     }
     idx_hi = __reduce_max_sync(0xffffffffu, idx_hi);
-    const bool uncl2 = hp.unc32 && idx_hi < 256u;                      // lut8 has 256 entries
-    const bool uncl3 = hp.unc32 && wtab && idx_hi < (uint32_t)ntab;  // zero-extended row table
-    // Float (denormal) form of the index map (params.cuh float_idx_ok): valid for this
-    // warp's unclipped range (flu) / for clipped distances (flc).  The integer distance
-    // delta = m - a (< 2^23 for d <= 256), read as an f32 bit pattern, IS the denormal
-    // delta * 2^-149, so one FMA with a denormal addend A * 2^-149 leaves
-    // round(delta * r) + A in the result's bit pattern: a shared-memory address.
-    const float rf = hp.fratio;  // 0: c_eff too large for the float form
-    const bool flu = IA_FLOAT_IDX && rf != 0.0f && float_idx_ok(hp.c_eff, (int64_t)idx_hi);
-    const bool flc = IA_FLOAT_IDX && rf != 0.0f && float_idx_ok(hp.c_eff, (int64_t)k);
-    const float rf9 = rf * 512.0f;  // pass 3: idx * 512 + 9 fraction bits
-    const float lutden = __uint_as_float(smem_u32(lut8));  // pass 2 addend: &lut8[0]
-    const uint32_t mI = (uint32_t)m;
+    const bool uncl2 = !flc && hp.unc32 && idx_hi < 256u;                      // lut8 has 256 entries
+    const bool uncl3 = !flc && hp.unc32 && wtab && idx_hi < (uint32_t)ntab;  // zero-extended row table
+    // Float form: u = max(a - lo, 0) = c_eff - delta' (one VIADDMNMX, the clip comes free),
+    // read as an f32 bit pattern, IS the denormal u * 2^-149; one FMA with a denormal addend
+    // A * 2^-149 leaves j + A in the result's bit pattern, j = k - idx: a shared-memory
+    // address into the reversed LUT (pass 2) / reversed row table (pass 3).
+    const float rf9 = rf * 512.0f;  // pass 3: j * 512 + 9 fraction bits
+    const float lutden = __uint_as_float(smem_u32(lut8r));  // pass 2 addend: &lut8r[0]
+    const int32_t nlo = (int32_t)(hp.c_eff - (int64_t)m);    // -lo (flc: |lo| < 2^31)
 
     // ---- pass 2: idx, e = lut[idx], S = sum e (softmax.py:144-155)
     uint32_t S = 0;
@@ -1030,21 +1043,16 @@ __global__ void __launch_bounds__(Cfg<DP>::NTHREADS, 1)
             }
           }
           const bool unc = uncl2 && !any_cut;
-          if ((unc && flu) || flc) {
-            // RN(delta * r + &lut8) in denormal units: the bit pattern is &lut8[idx]
-            auto fsum = [&](auto clip) {
-              const int32_t lo = im.lo;
+          if (flc) {
+            // RN(u * r + &lut8r) in denormal units: the bit pattern is &lut8r[k - idx]
 #pragma unroll
-              for (int e = 0; e < 32; ++e) {
-                const uint32_t xa = decltype(clip)::value ? (uint32_t)max((int32_t)va[e], lo) : va[e];
-                const uint32_t xb = decltype(clip)::value ? (uint32_t)max((int32_t)vb[e], lo) : vb[e];
-                float fa, fb;
-                fma_rn_f32x2(fa, fb, __uint_as_float(mI - xa), __uint_as_float(mI - xb), rf, lutden);
-                S += lds_u8(__float_as_uint(fa)) + lds_u8(__float_as_uint(fb));
-              }
-            };
-            if (unc && flu) fsum(std::false_type{});
-            else fsum(std::true_type{});
+            for (int e = 0; e < 32; ++e) {
+              const uint32_t ua = (uint32_t)__viaddmax_s32((int32_t)va[e], nlo, 0);
+              const uint32_t ub = (uint32_t)__viaddmax_s32((int32_t)vb[e], nlo, 0);
+              float fa, fb;
+              fma_rn_f32x2(fa, fb, __uint_as_float(ua), __uint_as_float(ub), rf, lutden);
+              S += lds_u8(__float_as_uint(fa)) + lds_u8(__float_as_uint(fb));
+            }
           } else if (unc) {
 #pragma unroll
             for (int e = 0; e < 32; ++e)
@@ -1089,8 +1097,10 @@ __global__ void __launch_bounds__(Cfg<DP>::NTHREADS, 1)
           q += r < 0 ? -1 : (r >= (int32_t)two_s ? 1 : 0);
           pv = (uint32_t)q;
         }
-        if (wtab) reinterpret_cast<uint32_t*>(tab)[t * 128 + row] = pv;
-        else tab[t * 128 + row] = (uint8_t)pv;
+        // float form: entry j = k - t (entries past k are never addressed: u <= c_eff)
+        const int tt = flc ? (t <= (int)k ? (int)k - t : t) : t;
+        if (wtab) reinterpret_cast<uint32_t*>(tab)[tt * 128 + row] = pv;
+        else tab[tt * 128 + row] = (uint8_t)pv;
       }
     }
     named_bar_sync(1, NWT);
@@ -1109,7 +1119,7 @@ __global__ void __launch_bounds__(Cfg<DP>::NTHREADS, 1)
     // Only rows long enough for P^ to be sparse pay the per-row scan (n_kt >= 16);
     // shorter rows keep theta = INT_MIN (no group is skipped).
     int32_t theta = n_kt >= 16 ? INT_MAX : INT_MIN;
-    if (!QO && m9 && n_kt >= 16 && row_valid && !dead && S) {
+    if (!QO && (m9 || flc) && n_kt >= 16 && row_valid && !dead && S) {
       int tstar = -1;
       for (int t = 0; t < nlut; ++t)
         if ((uint32_t)p.scale_x2 * (uint32_t)lut8[t] >= S) tstar = t;
@@ -1193,13 +1203,11 @@ __global__ void __launch_bounds__(Cfg<DP>::NTHREADS, 1)
           }
           const bool unc = uncl3 && !any_cut;
           if (!live) {
-          } else if ((unc && flu) || flc) {
-            // RZ(delta * 512 r + tab0 + 256) in denormal units: tab0 + idx * 512 + 9 fraction
-            // bits; the row-table address is one LOP3 away (as with magic9)
-            // addend: (tab0 + 256) * 2^-149 (the 256 is the map's + 1/2 in units of 1/512)
+          } else if (flc) {
+            // RZ(u * 512 r + tab0 + 256) in denormal units: tab0 + (k - idx) * 512 + 9
+            // fraction bits; the (reversed) row-table address is one LOP3 away
             const float tabden = __uint_as_float(tab0 + 256u);
-            const int32_t lo = im.lo;
-            auto fgroups = [&](auto clip, auto skip) {
+            auto fgroups = [&](auto skip) {
               constexpr int G = IA_SKIP_G;  // keys per skip group
 #pragma unroll
               for (int g = 0; g < 64 / G; ++g) {
@@ -1216,10 +1224,10 @@ __global__ void __launch_bounds__(Cfg<DP>::NTHREADS, 1)
                   uint32_t pw[4];
 #pragma unroll
                   for (int e = 0; e < 4; e += 2) {
-                    const uint32_t x0 = decltype(clip)::value ? (uint32_t)max((int32_t)v4[e], lo) : v4[e];
-                    const uint32_t x1 = decltype(clip)::value ? (uint32_t)max((int32_t)v4[e + 1], lo) : v4[e + 1];
+                    const uint32_t u0 = (uint32_t)__viaddmax_s32((int32_t)v4[e], nlo, 0);
+                    const uint32_t u1 = (uint32_t)__viaddmax_s32((int32_t)v4[e + 1], nlo, 0);
                     float f0, f1;
-                    fma_rz_f32x2(f0, f1, __uint_as_float(mI - x0), __uint_as_float(mI - x1), rf9, tabden);
+                    fma_rz_f32x2(f0, f1, __uint_as_float(u0), __uint_as_float(u1), rf9, tabden);
                     pw[e] = lds_u32(and_or(__float_as_uint(f0), 0xFFFFFE00u, row4));
                     pw[e + 1] = lds_u32(and_or(__float_as_uint(f1), 0xFFFFFE00u, row4));
                   }
@@ -1228,14 +1236,8 @@ __global__ void __launch_bounds__(Cfg<DP>::NTHREADS, 1)
                 }
               }
             };
-            const bool skip = IA_GROUP_SKIP && n_kt >= 16;
-            if (unc && flu) {
-              if (skip) fgroups(std::false_type{}, std::true_type{});
-              else fgroups(std::false_type{}, std::false_type{});
-            } else {
-              if (skip) fgroups(std::true_type{}, std::true_type{});
-              else fgroups(std::true_type{}, std::false_type{});
-            }
+            if (IA_GROUP_SKIP && n_kt >= 16) fgroups(std::true_type{});
+            else fgroups(std::false_type{});
           } else if (m9) {
             // address = tab0 + ((umulhi(n, magic9) & ~511) | row*4): IMAD, IMAD.HI, LOP3,
             // LDS per logit (+ the clip VIMNMX when the warp's index range exceeds the

@@ -38,52 +38,49 @@ __host__ __device__ inline int bitlen_u64(uint64_t x) {
 
 // Float form of the same index map (the fused kernel's fast path for small c_eff).
 //
-// idx = floor((2k*delta + c) / (2c)) = floor(y0 + 1/2), y0 = delta * k / c (c = c_eff).
-// With r = the smallest f32 strictly above k/c (r = (k/c)(1 + eps), 0 < eps <= 2^-23)
-// one FMA computes y = delta * r = y0 (1 + eps) exactly before its single rounding.
-// y0 is a multiple of 1/c, so the half-integer above it is at least 1/(2c) away; with
-// y0 <= B + 1/2 (B = the largest index the caller can reach) and  c (2B + 1) < 2^23
-// the excess y0 * eps stays below that gap:
-//   T - 1/2 < y < T + 1/2  (or y > y0 = T - 1/2 on an exact tie),  T = floor(y0 + 1/2).
-// The kernel feeds the FMA the integer delta (< 2^23) reinterpreted as an f32: that bit
-// pattern is the denormal delta * 2^-149, and with a denormal addend A * 2^-149 the
-// result RN(y + A) * 2^-149 has the bit pattern T + A (pass 2: A = &lut8, the bits are the
-// LUT address), RZ(512 y + 256 + A) the pattern A + 512 T + (9 fraction bits) (pass 3: A =
-// the row table, one LOP3 from the entry address, as with magic9).  Denormal FMAs run at
-// full rate and pack two lanes per instruction (FFMA2): measured 2x (pass 2) and 1.6x
-// (pass 3) the throughput of the IMAD / IMAD.HI form (tools/loop_bench.cu).
-// Exhaustive check: tests/test_kernel_arith.py.
-__host__ __device__ inline bool float_idx_ok(int64_t c_eff, int64_t max_idx) {
-  return c_eff > 0 && max_idx >= 0 && max_idx < (int64_t(1) << 22) &&
-         c_eff < (int64_t(1) << 23) && c_eff * (2 * max_idx + 1) < (int64_t(1) << 23);
+// With lo = m - c (c = c_eff) and u = max(a - lo, 0) = c - delta' in [0, c] (one VIADDMNMX;
+// the clip comes free),
+//   idx = floor((2k*delta' + c) / (2c)) = k - j,   j = floor((2k*u + c - 1) / (2c))
+//       = floor(y0 + 1/2 - 1/(2c)),  y0 = u * k / c:
+// j is y0 rounded to the nearest integer with ties going DOWN.  Let r be the largest f32
+// strictly below k/c (r = (k/c)(1 - eps), 0 < eps <= 2^-23).  One FMA computes y = u * r =
+// y0 (1 - eps) exactly before its single rounding.  y0 + 1/2 is a multiple of 1/(2c), so
+// off a tie y0 is at least 1/(2c) above the half-integer below it, and with  c (2k + 1) <
+// 2^23  the deficit y0 * eps <= k * 2^-23 stays below that gap:  T - 1/2 < y < T + 1/2 with
+// T = j; on a tie (y0 = T + 1/2) y is strictly below T + 1/2, so it rounds down to T = j.
+// The kernel feeds the FMA the integer u (< 2^23) reinterpreted as an f32: that bit pattern
+// is the denormal u * 2^-149, and with a denormal addend A * 2^-149 the result
+// RN(y + A) * 2^-149 has the bit pattern j + A (pass 2: A = the address of a reversed LUT,
+// lutr[j] = lut[k - j], so the bits are the entry's address), RZ(512 y + 256 + A) the
+// pattern A + 512 j + (9 fraction bits) (pass 3: A = the reversed row table, one LOP3 from
+// the entry address, as with magic9).  Denormal FMAs run at full rate and pack two lanes
+// per instruction (FFMA2): measured 2x (pass 2) and 1.6x (pass 3) the throughput of the
+// IMAD / IMAD.HI form (tools/loop_bench.cu).  Exhaustive check: tests/test_kernel_arith.py.
+__host__ __device__ inline bool float_idx_ok(int64_t c_eff, int64_t k) {
+  return c_eff > 0 && k > 0 && k < 256 && c_eff < (int64_t(1) << 23) &&
+         c_eff * (2 * k + 1) < (int64_t(1) << 23);
 }
-// Smallest f32 strictly above k / c_eff (c_eff < 2^23: the products below are exact in f64).
+// Largest f32 strictly below k / c_eff (c_eff < 2^23: the products below are exact in f64).
 __host__ __device__ inline float float_idx_ratio(int64_t c_eff, int64_t k) {
   const double rd = (double)k / (double)c_eff;
-  float r = (float)rd;  // round to nearest, then step up until r * c_eff > k
+  float r = (float)rd;  // round to nearest, then step down until r * c_eff < k
   uint32_t bits;
 #ifdef __CUDA_ARCH__
   bits = __float_as_uint(r);
 #else
   memcpy(&bits, &r, 4);
 #endif
-  for (int it = 0; it < 3; ++it) {
+  for (int it = 0; it < 4; ++it) {
     float f;
 #ifdef __CUDA_ARCH__
     f = __uint_as_float(bits);
 #else
     memcpy(&f, &bits, 4);
 #endif
-    if ((double)f * (double)c_eff > (double)k) return f;
-    ++bits;
+    if ((double)f * (double)c_eff < (double)k) return f;
+    --bits;
   }
-  float f;
-#ifdef __CUDA_ARCH__
-  f = __uint_as_float(bits);
-#else
-  memcpy(&f, &bits, 4);
-#endif
-  return f;
+  return 0.0f;  // unreachable for k >= 1
 }
 
 // Fill everything except the scales.  k = nlut - 1.
@@ -141,7 +138,7 @@ __host__ __device__ inline void fill_head_params(int64_t c_int, int64_t dbound, 
     }
   }
   if (!hp->use32) hp->unc32 = 0;
-  hp->fratio = (hp->use32 && float_idx_ok(c_eff, 0)) ? float_idx_ratio(c_eff, k) : 0.0f;
+  hp->fratio = (hp->use32 && float_idx_ok(c_eff, k)) ? float_idx_ratio(c_eff, k) : 0.0f;
   // Scaled magic for every n whose index fits the fused kernel's zero-extended row
   // table (idx <= NT9 = row_table_entries(nlut) - 1: n < 2 c_eff (NT9 + 1)), which
   // covers the clipped range n <= (2k+1) c_eff and the unclipped n of any row whose

@@ -36,53 +36,40 @@ def _float_ratio_parts(r):
 
 
 def test_float_index_map_exact():
-    """params.cuh float form of idx = (2k*delta + c) // (2c): the fused kernel reads the
-    integer delta as the f32 denormal delta * 2^-149 and takes RN(delta * r + A) (pass 2)
-    or RZ(delta * 512 r + 256 + A) >> 9 (pass 3) from one FMA.  Both are checked here in
-    exact integer arithmetic for every distance the kernel can feed them, with the ratio
-    the library itself computes (ia_head_params.fratio)."""
+    """params.cuh float form of idx = (2k*delta' + c) // (2c): with u = c - delta' =
+    max(a - (m - c), 0) the kernel reads the integer u as the f32 denormal u * 2^-149 and
+    takes j = RN(u * r + A) (pass 2) or RZ(u * 512 r + 256 + A) >> 9 (pass 3) from one FMA,
+    idx = k - j.  Both are checked here in exact integer arithmetic for EVERY u in [0, c]
+    with the ratio the library itself computes (ia_head_params.fratio)."""
     from paper_2511_21513_b200 import _lib
 
     rng = np.random.default_rng(7)
-    for b in (2, 3, 5, 6, 8):
+    for b in (2, 3, 5, 6):
         nlut = 1 << b
         k = nlut - 1
-        c_values = [1, 2, 3, 7, 31, 62, 587, 660, 5233, 37474, 48161, 54498]
-        c_values += [(1 << 23) // (2 * k + 1) - j for j in (0, 1, 2)]  # largest c_eff with flc
-        c_values += [int(x) for x in rng.integers(1, (1 << 23) // (2 * k + 1), size=8)]
-        c_values += [31 * (1 << j) for j in range(0, 12)]  # k / c exactly representable for b = 5
+        cmax = ((1 << 23) - 1) // (2 * k + 1)          # largest c_eff with c (2k + 1) < 2^23
+        c_values = [1, 2, 3, 7, 31, 62, 587, 660, 5233, 37474, 48161, 54498, cmax, cmax - 1, cmax + 1,
+                    cmax + 2, 1 << 22, (1 << 23) - 1, 1 << 23]
+        c_values += [int(x) for x in rng.integers(1, cmax + 1, size=8)]
+        c_values += [k * (1 << j) for j in range(0, 14)]  # k / c exactly representable
         for c in c_values:
             hp = _lib.softmax_params_host(c, 2 * 256 * 127 * 127, nlut)
             c_eff = int(hp.c_eff)
             r = np.float32(hp.fratio)
-            if not (c_eff < (1 << 23) and hp.use32):
-                assert r == 0
+            if not (hp.use32 and c_eff * (2 * k + 1) < (1 << 23)):
+                assert r == 0, (b, c)
                 continue
-            assert r > 0 and np.float64(r) * c_eff > k  # strictly above k / c_eff ...
-            below = np.nextafter(r, np.float32(0))
-            assert np.float64(below) * c_eff <= k        # ... and the smallest such f32
+            assert r > 0 and np.float64(r) * c_eff < k   # strictly below k / c_eff ...
+            above = np.nextafter(r, np.float32(np.inf))
+            assert np.float64(above) * c_eff >= k         # ... and the largest such f32
             R, E = _float_ratio_parts(r)
-            # largest reachable index B with c_eff * (2B + 1) < 2^23 (float_idx_ok), and
-            # every delta whose exact index is <= B (the warp's unclipped range) or <= c_eff
-            B = ((1 << 23) // c_eff - 1) // 2
-            if c_eff * (2 * B + 1) >= (1 << 23):
-                B -= 1
-            if B < 0:
-                continue
-            top = min((c_eff * (2 * B + 1) - 1) // (2 * k), (1 << 23) - 1)
-            if B >= k:
-                top = max(top, c_eff)
-            if top <= 2_000_000:
-                d = np.arange(0, top + 1, dtype=np.int64)
-            else:
-                d = np.unique(np.concatenate([rng.integers(0, top + 1, 1_500_000),
-                                              np.arange(0, 2000), np.arange(top - 2000, top + 1)]))
-            want = (2 * k * d + c_eff) // (2 * c_eff)
-            assert int(want.max()) <= max(B, 0) or B >= k
-            prod = d * R  # < 2^47
+            u = np.arange(0, c_eff + 1, dtype=np.int64)   # every clipped distance, reversed
+            delta = c_eff - u
+            want = (2 * k * delta + c_eff) // (2 * c_eff)
+            prod = u * R  # < 2^47
             q, rem = prod >> E, prod & ((1 << E) - 1)
             half = 1 << (E - 1)
             rn = q + ((rem > half) | ((rem == half) & (q & 1 == 1)))
-            assert np.array_equal(rn, want), (b, c, "RN form")
+            assert np.array_equal(k - rn, want), (b, c, "RN form")
             rz = ((prod.astype(np.uint64) << np.uint64(9)) + (np.uint64(256) << np.uint64(E))) >> np.uint64(E)
-            assert np.array_equal((rz >> np.uint64(9)).astype(np.int64), want), (b, c, "RZ form")
+            assert np.array_equal(k - (rz >> np.uint64(9)).astype(np.int64), want), (b, c, "RZ form")
