@@ -237,6 +237,30 @@ __device__ __forceinline__ void bwait(uint64_t* bar, uint32_t parity, bool spin)
 #ifndef IA_SKIP_G
 #define IA_SKIP_G 8
 #endif
+// pass-3 skip decisions for a whole 64-key batch at once (see fgroups)
+#ifndef IA_SKIP_MASK
+#define IA_SKIP_MASK 1
+#endif
+// pass-1 row max: independent VIMNMX3 chains per 64-logit batch
+// timing-only experiments (never in a shipped build; results are wrong with any bit set):
+// 1 pass 2 without its LUT gather, 2 pass 3 without its row-table gather, 4 no P^ stores,
+// 8 K producer arrives without loading (stale K tiles)
+#ifndef IA_EXP
+#define IA_EXP 0
+#endif
+// warp id made provably uniform (shuffle from lane 0): role loops on the uniform datapath
+// (476 -> 77 R2UR, four back-to-back UTCIMMA per tile) -- measured 3-5 % SLOWER on C4
+// (2.585 -> 2.68 / 2.72 ms), so off
+#ifndef IA_UNIFORM_WARP
+#define IA_UNIFORM_WARP 0
+#endif
+// rows of at least this many key tiles use the pass-3 group skip
+#ifndef IA_SKIP_MIN_KT
+#define IA_SKIP_MIN_KT 16
+#endif
+#ifndef IA_P1_CHAINS
+#define IA_P1_CHAINS 2
+#endif
 #ifndef IA_PRODUCER_BACKOFF_NS
 #define IA_PRODUCER_BACKOFF_NS 0
 #endif
@@ -528,13 +552,20 @@ __global__ void __launch_bounds__(Cfg<DP>::NTHREADS, 1)
   const int kvh = b * p.Hkv + h / (p.H / p.Hkv);
   const int q0 = qt * BM;
   const int len = p.seq_lens ? min(p.seq_lens[b], p.L) : p.L;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  // warp id through a shuffle from lane 0: ptxas then knows it is warp-uniform, so the role
+  // branches are uniform branches and the role loops (barrier addresses, smem descriptors,
+  // ring counters) run on the uniform datapath instead of R2UR moves per MMA -- the issue
+  // loops compete for issue slots with three softmax warps on their SM sub-partition
+  const int warp_u = IA_UNIFORM_WARP ? __shfl_sync(0xffffffffu, (int)(threadIdx.x >> 5), 0) : (int)(threadIdx.x >> 5);
+  // IA_UNIFORM_WARP 2: only the role dispatch sees the uniform id (softmax code unchanged)
+  const int warp = IA_UNIFORM_WARP == 1 ? warp_u : (int)(threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
   // Softmax warpgroups are warps 0 .. 4*NWG-1; the four role warps come last.  The
   // warp scheduler favours the highest warp id among eligible warps, so the
   // latency-critical TMA / MMA issue loops win their issue slots over the
   // arithmetic-heavy softmax warps sharing their SM sub-partition.
   // role: 0 K producer, 1 QK^T, 2 V^T producer + TMEM alloc, 3 P.V; < 0: softmax warp
-  const int rw = IA_ROLE_FIRST ? (warp < 4 ? warp : -1) : warp - 4 * NWG;
+  const int rw = IA_ROLE_FIRST ? (warp_u < 4 ? warp_u : -1) : warp_u - 4 * NWG;
   const int sw = IA_ROLE_FIRST ? warp - 4 : warp;  // softmax warp index (when rw < 0)
   const int stid = IA_ROLE_FIRST ? (int)threadIdx.x - 128 : (int)threadIdx.x;
 
@@ -584,7 +615,7 @@ __global__ void __launch_bounds__(Cfg<DP>::NTHREADS, 1)
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
-  const uint32_t tmem = *tmem_slot;
+  const uint32_t tmem = IA_UNIFORM_WARP ? __shfl_sync(0xffffffffu, *tmem_slot, 0) : *tmem_slot;
   int trc = 0;  // trace entry counter (IA_TRACE)
   (void)trc;
   long long tacc[8] = {0, 0, 0, 0, 0, 0, 0, 0};  // IA_TADD slots 8..15
@@ -613,6 +644,9 @@ __global__ void __launch_bounds__(Cfg<DP>::NTHREADS, 1)
     for (int t = 0; t < nloads; ++t) {
       pwait(k_empty + ks, ((kph >> ks) & 1u) ^ 1u, XF(16));
       kph ^= 1u << ks;
+      if ((IA_EXP & 8) && t >= C::NKX) {
+        if (elect_one()) mbar_arrive(k_full + ks);
+      } else
       if (elect_one()) {
         IA_TRACE(0, 1, t);
         mbar_expect_tx(k_full + ks, C::K_BYTES);
@@ -655,7 +689,7 @@ __global__ void __launch_bounds__(Cfg<DP>::NTHREADS, 1)
     // one pass at a time; within a pass tile n uses K stage n % RING and buffer n % NWG,
     // so an unrolled round over the ring has every barrier, descriptor and TMEM column
     // offset as a compile-time constant
-    const uint32_t tm = *tmem_slot;  // re-read: keeps the loop free of a spilled reload
+    const uint32_t tm = IA_UNIFORM_WARP ? tmem : *tmem_slot;  // (re-read: keeps the loop free of a spilled reload)
     // s_free parity starts at 1: a fresh barrier counts its (nonexistent) previous
     // phase as complete, so every buffer's first use passes without a special case
     uint32_t f_ph = (1u << NWG) - 1u;
@@ -907,7 +941,17 @@ __global__ void __launch_bounds__(Cfg<DP>::NTHREADS, 1)
           if (!__any_sync(0xffffffffu, cut < 64)) {
             // two 3-input VIMNMX3 chains per direction: one instruction per two logits
             int32_t mx1 = mx, mn1 = mn;
-            if (flc) {
+            if (flc && IA_P1_CHAINS == 4) {
+              int32_t mx2 = mx, mx3 = mx;
+#pragma unroll
+              for (int e = 0; e < 16; e += 2) {
+                mx = __vimax3_s32(mx, (int32_t)va[e], (int32_t)va[e + 1]);
+                mx1 = __vimax3_s32(mx1, (int32_t)vb[e], (int32_t)vb[e + 1]);
+                mx2 = __vimax3_s32(mx2, (int32_t)va[e + 16], (int32_t)va[e + 17]);
+                mx3 = __vimax3_s32(mx3, (int32_t)vb[e + 16], (int32_t)vb[e + 17]);
+              }
+              mx = __vimax3_s32(mx, mx2, mx3);
+            } else if (flc) {
 #pragma unroll
               for (int e = 0; e < 32; e += 2) {
                 mx = __vimax3_s32(mx, (int32_t)va[e], (int32_t)va[e + 1]);
@@ -1051,7 +1095,8 @@ __global__ void __launch_bounds__(Cfg<DP>::NTHREADS, 1)
               const uint32_t ub = (uint32_t)__viaddmax_s32((int32_t)vb[e], nlo, 0);
               float fa, fb;
               fma_rn_f32x2(fa, fb, __uint_as_float(ua), __uint_as_float(ub), rf, lutden);
-              S += lds_u8(__float_as_uint(fa)) + lds_u8(__float_as_uint(fb));
+              if (IA_EXP & 1) S += (__float_as_uint(fa) & 255u) + (__float_as_uint(fb) & 255u);
+              else S += lds_u8(__float_as_uint(fa)) + lds_u8(__float_as_uint(fb));
             }
           } else if (unc) {
 #pragma unroll
@@ -1116,10 +1161,10 @@ __global__ void __launch_bounds__(Cfg<DP>::NTHREADS, 1)
     // i.e. only for logits a >= theta = m - T + 1.  A group of keys whose largest logit
     // is below theta in every row of the warp is all zero.  Scans every LUT entry, so
     // it holds for any LUT (no monotonicity assumed).
-    // Only rows long enough for P^ to be sparse pay the per-row scan (n_kt >= 16);
+    // Only rows long enough for P^ to be sparse pay the per-row scan (n_kt >= IA_SKIP_MIN_KT);
     // shorter rows keep theta = INT_MIN (no group is skipped).
-    int32_t theta = n_kt >= 16 ? INT_MAX : INT_MIN;
-    if (!QO && (m9 || flc) && n_kt >= 16 && row_valid && !dead && S) {
+    int32_t theta = n_kt >= IA_SKIP_MIN_KT ? INT_MAX : INT_MIN;
+    if (!QO && (m9 || flc) && n_kt >= IA_SKIP_MIN_KT && row_valid && !dead && S) {
       int tstar = -1;
       for (int t = 0; t < nlut; ++t)
         if ((uint32_t)p.scale_x2 * (uint32_t)lut8[t] >= S) tstar = t;
@@ -1209,10 +1254,28 @@ __global__ void __launch_bounds__(Cfg<DP>::NTHREADS, 1)
             const float tabden = __uint_as_float(tab0 + 256u);
             auto fgroups = [&](auto skip) {
               constexpr int G = IA_SKIP_G;  // keys per skip group
+              // IA_SKIP_MASK: all group maxima first (64 / G independent chains), one
+              // warp-wide OR of the per-lane live bits, then uniform branches -- instead
+              // of a max chain + vote + branch per group (a serial ~45-cycle chain each)
+              uint32_t live_groups = 0xffffffffu;
+              if (decltype(skip)::value && IA_SKIP_MASK) {
+                uint32_t lm = 0u;
+#pragma unroll
+                for (int g = 0; g < 64 / G; ++g) {
+                  const uint32_t* vg = g < 32 / G ? &va[G * g] : &vb[G * (g - 32 / G)];
+                  int32_t gm = (int32_t)vg[0];
+#pragma unroll
+                  for (int e = 1; e < G; ++e) gm = max(gm, (int32_t)vg[e]);
+                  lm |= gm >= theta ? (1u << g) : 0u;
+                }
+                live_groups = __reduce_or_sync(0xffffffffu, lm);
+              }
 #pragma unroll
               for (int g = 0; g < 64 / G; ++g) {
                 const uint32_t* vg = g < 32 / G ? &va[G * g] : &vb[G * (g - 32 / G)];
-                if (decltype(skip)::value) {
+                if (decltype(skip)::value && IA_SKIP_MASK) {
+                  if (!((live_groups >> g) & 1u)) continue;  // pk stays 0
+                } else if (decltype(skip)::value) {
                   int32_t gm = (int32_t)vg[0];
 #pragma unroll
                   for (int e = 1; e < G; ++e) gm = max(gm, (int32_t)vg[e]);
@@ -1228,15 +1291,20 @@ __global__ void __launch_bounds__(Cfg<DP>::NTHREADS, 1)
                     const uint32_t u1 = (uint32_t)__viaddmax_s32((int32_t)v4[e + 1], nlo, 0);
                     float f0, f1;
                     fma_rz_f32x2(f0, f1, __uint_as_float(u0), __uint_as_float(u1), rf9, tabden);
+                    if (IA_EXP & 2) {
+                      pw[e] = and_or(__float_as_uint(f0), 0xFFFFFE00u, row4) >> 9;
+                      pw[e + 1] = and_or(__float_as_uint(f1), 0xFFFFFE00u, row4) >> 9;
+                    } else {
                     pw[e] = lds_u32(and_or(__float_as_uint(f0), 0xFFFFFE00u, row4));
                     pw[e + 1] = lds_u32(and_or(__float_as_uint(f1), 0xFFFFFE00u, row4));
+                    }
                   }
                   pk[(G / 4) * g + q] = __byte_perm(__byte_perm(pw[0], pw[1], 0x0040),
                                                     __byte_perm(pw[2], pw[3], 0x0040), 0x5410);
                 }
               }
             };
-            if (IA_GROUP_SKIP && n_kt >= 16) fgroups(std::true_type{});
+            if (IA_GROUP_SKIP && n_kt >= IA_SKIP_MIN_KT) fgroups(std::true_type{});
             else fgroups(std::false_type{});
           } else if (m9) {
             // address = tab0 + ((umulhi(n, magic9) & ~511) | row*4): IMAD, IMAD.HI, LOP3,
@@ -1271,7 +1339,7 @@ __global__ void __launch_bounds__(Cfg<DP>::NTHREADS, 1)
             };
             // short rows (theta = INT_MIN) take the branch-free form: all 64 logits
             // interleave freely
-            const bool skip = IA_GROUP_SKIP && n_kt >= 16;
+            const bool skip = IA_GROUP_SKIP && n_kt >= IA_SKIP_MIN_KT;
             if (unc) {
               if (skip) groups(std::false_type{}, std::true_type{});
               else groups(std::false_type{}, std::false_type{});
@@ -1314,6 +1382,7 @@ __global__ void __launch_bounds__(Cfg<DP>::NTHREADS, 1)
 #pragma unroll
         for (int u = 0; u < 4; ++u) {  // 16-byte units 4*hb + u of this row
           const uint32_t x = (uint32_t)(4 * hb + u);
+          if (!(IA_EXP & 4) || ((pk[4 * u] ^ pk[4 * u + 1] ^ pk[4 * u + 2] ^ pk[4 * u + 3]) == 0x12345u))
           sts128(p_row + ((x ^ p_xor) << 4), pk[4 * u], pk[4 * u + 1], pk[4 * u + 2], pk[4 * u + 3]);
         }
       }
