@@ -1132,7 +1132,11 @@ __global__ void __launch_bounds__(Cfg<DP>::NTHREADS, 1)
       // of the exact one, so one remainder check makes it the exact floor
       const uint32_t two_s = 2u * S;
       const float rden = S ? __frcp_rn((float)two_s) : 0.0f;
-      for (int t = wg; t < ntab; t += NWG) {  // lut8[t] = 0 (incl. t >= nlut) -> S / 2S = 0
+      // float form: only entries j = k - t, t <= k, are ever addressed (u <= c_eff), so the
+      // zero-extension of the integer form's table is not built (short rows: the table
+      // build is a fixed cost per CTA)
+      const int nbuild = flc ? nlut : ntab;
+      for (int t = wg; t < nbuild; t += NWG) {  // lut8[t] = 0 (incl. t >= nlut) -> S / 2S = 0
         const uint32_t lt = lut8[t];
         uint32_t pv = 0u;
         if (S && lt) {
