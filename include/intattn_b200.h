@@ -132,7 +132,9 @@ int ia_head_params_host(double c, int64_t d, int nlut, int p_scale, float s_q, f
 /* Index map of one (query head, key group) of the grouped-K fused kernel: c_eff and
  * the magic numbers of ia_head_params for c_int = round(c / alpha_g), alpha_g =
  * f64(s_q) f64(s_k[g]) / sqrt(d) (softmax.py:370-378).  A group whose c_eff does
- * not fit 31 bits has idx = 0 for every reachable delta and is stored as magic 0. */
+ * not fit 31 bits has idx = 0 for every reachable delta and is stored as magic 0.
+ * use32 bit 1 set: c_eff (2k + 1) < 2^23, the kernel uses the float form of the map
+ * and `magic` holds the bits of its f32 ratio (the largest f32 below k / c_eff). */
 typedef struct ia_group_params {
   int32_t c_eff;
   uint32_t magic;

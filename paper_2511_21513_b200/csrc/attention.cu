@@ -304,15 +304,26 @@ __device__ __forceinline__ void gk_group_max(const AttnDev& p, uint32_t s_tile, 
     const int j0 = j0t + hb * 64;
     const uint32_t ma = gk_mask32(p, row_valid, i, j0, lim);
     const uint32_t mb = gk_mask32(p, row_valid, i, j0 + 32, lim);
+    if (!__any_sync(0xffffffffu, (ma | mb) != 0u)) {  // no key masked in the warp: plain maxima
 #pragma unroll
-    for (int c = 0; c < 8; ++c) {
-      const uint32_t* v8 = c < 4 ? &va[8 * c] : &vb[8 * (c - 4)];
-      const uint32_t bits = ((c < 4 ? ma : mb) >> (8 * (c & 3))) & 0xffu;
-      int32_t x = INT_MIN;
+      for (int c = 0; c < 8; ++c) {
+        const uint32_t* v8 = c < 4 ? &va[8 * c] : &vb[8 * (c - 4)];
+        int32_t x = __vimax3_s32((int32_t)v8[0], (int32_t)v8[1], (int32_t)v8[2]);
+        x = __vimax3_s32(x, (int32_t)v8[3], (int32_t)v8[4]);
+        x = __vimax3_s32(x, (int32_t)v8[5], (int32_t)v8[6]);
+        gm[hb * 8 + c] = max(x, (int32_t)v8[7]);
+      }
+    } else {
 #pragma unroll
-      for (int e = 0; e < 8; ++e)
-        if (!((bits >> e) & 1u)) x = max(x, (int32_t)v8[e]);
-      gm[hb * 8 + c] = x;
+      for (int c = 0; c < 8; ++c) {
+        const uint32_t* v8 = c < 4 ? &va[8 * c] : &vb[8 * (c - 4)];
+        const uint32_t bits = ((c < 4 ? ma : mb) >> (8 * (c & 3))) & 0xffu;
+        int32_t x = INT_MIN;
+#pragma unroll
+        for (int e = 0; e < 8; ++e)
+          if (!((bits >> e) & 1u)) x = max(x, (int32_t)v8[e]);
+        gm[hb * 8 + c] = x;
+      }
     }
   }
   // chunks of one group share its maximum (groups of gs/8 = 1..16 chunks)
@@ -358,7 +369,8 @@ struct GkMap {
 
 template <int DP, bool DEBUG>
 __device__ __forceinline__ void gk_passes(const AttnDev& p, uint8_t* smem, uint32_t* tab,
-                                          uint32_t* xsum, const uint8_t* lut8, uint64_t* s_full,
+                                          uint32_t* xsum, const uint8_t* lut8, const uint8_t* lut8r,
+                                          uint64_t* s_full,
                                           uint64_t* s_free, uint64_t* p_full, uint64_t* p_free,
                                           uint32_t s_base, int wg, int row, int lane, int i,
                                           int lim, int bh, int n_kt, bool row_valid,
@@ -371,6 +383,7 @@ __device__ __forceinline__ void gk_passes(const AttnDev& p, uint8_t* smem, uint3
   uint32_t nk2 = 0u - 2u * k;
   asm("" : "+r"(nk2));
   const int4* gp = p.kgroup + (size_t)bh * p.n_groups;
+  const float lutden = __uint_as_float(smem_u32(lut8r));  // float form, pass A addend: &lut8r[0]
 
   // ---- pass A: e = lut[idx_g], S = sum e (softmax.py:380-394); the only wait on the
   // MMA when the logits stay resident in TMEM
@@ -398,11 +411,32 @@ __device__ __forceinline__ void gk_passes(const AttnDev& p, uint8_t* smem, uint3
       for (int c = 0; c < 8; ++c) {
         const int32_t gmax = hb ? gm[8 + c] : gm[c];
         if (gmax == INT_MIN) continue;  // every key of the chunk is masked: e = 0
-        GkMap gmap;
-        gmap.init(gmax, __ldg(gp + ((j0 + 8 * c) >> p.gs_log2)), k);
+        const int4 gpar = __ldg(gp + ((j0 + 8 * c) >> p.gs_log2));
         const uint32_t* v8 = c < 4 ? &va[8 * c] : &vb[8 * (c - 4)];
         const uint32_t bits = ((c < 4 ? ma : mb) >> (8 * (c & 3))) & 0xffu;
-        if (open && gmap.use32) {  // warp-uniform: the common case, no per-key tests
+        if (gpar.w & 2) {
+          // float form (params.cuh, as the per-tensor kernel): u = max(a - lo_g, 0), one
+          // denormal FMA leaves &lut8r[k - idx] in the result's bits; masked keys take u = 0
+          // (idx = k, lut[k] = 0).  Warp-uniform: the group's parameters are.
+          const float rg = __int_as_float(gpar.y);
+          const int32_t nlo = gpar.x - gmax;
+#pragma unroll
+          for (int e = 0; e < 8; e += 2) {
+            uint32_t u0 = (uint32_t)__viaddmax_s32((int32_t)v8[e], nlo, 0);
+            uint32_t u1 = (uint32_t)__viaddmax_s32((int32_t)v8[e + 1], nlo, 0);
+            if (!open) {
+              u0 = ((bits >> e) & 1u) ? 0u : u0;
+              u1 = ((bits >> (e + 1)) & 1u) ? 0u : u1;
+            }
+            float f0, f1;
+            fma_rn_f32x2(f0, f1, __uint_as_float(u0), __uint_as_float(u1), rg, lutden);
+            S += lds_u8(__float_as_uint(f0)) + lds_u8(__float_as_uint(f1));
+          }
+          continue;
+        }
+        GkMap gmap;
+        gmap.init(gmax, gpar, k);
+        if (open && gmap.use32) {  // warp-uniform: no per-key tests
 #pragma unroll
           for (int e = 0; e < 8; ++e) S += lut8[gmap.idx32((int32_t)v8[e], nk2)];
         } else {
@@ -432,13 +466,15 @@ __device__ __forceinline__ void gk_passes(const AttnDev& p, uint8_t* smem, uint3
         q += r < 0 ? -1 : (r >= (int32_t)two_s ? 1 : 0);
         pv = (uint32_t)q;
       }
-      tab[t * 128 + row] = pv;
+      tab[((int)k - t) * 128 + row] = pv;  // reversed: entry j = k - idx (the float form's index)
     }
   }
   named_bar_sync(1, NWT);
 
   // ---- pass B: P^ = rowtab[idx_g] -> smem -> P.V MMA
   const uint32_t tab_row = smem_u32(tab) + (uint32_t)row * 4u;
+  const uint32_t row4 = (uint32_t)row * 4u;
+  const float tabden = __uint_as_float(smem_u32(tab) + 256u);  // float form, pass B addend
   const uint32_t p_rows = smem_u32(smem + C::OFF_P + wg * C::NPB * C::P_BYTES) + (uint32_t)row * 128;
   const uint32_t p_xor = (uint32_t)(row & 7);
   int tl = 0;
@@ -473,24 +509,50 @@ __device__ __forceinline__ void gk_passes(const AttnDev& p, uint8_t* smem, uint3
       for (int c = 0; c < 8; ++c) {
         const int32_t gmax = hb ? gm[8 + c] : gm[c];
         if (gmax == INT_MIN) continue;
-        GkMap gmap;
-        gmap.init(gmax, __ldg(gp + ((j0 + 8 * c) >> p.gs_log2)), k);
+        const int4 gpar = __ldg(gp + ((j0 + 8 * c) >> p.gs_log2));
         const uint32_t* v8 = c < 4 ? &va[8 * c] : &vb[8 * (c - 4)];
         const uint32_t bits = ((c < 4 ? ma : mb) >> (8 * (c & 3))) & 0xffu;
+        if (gpar.w & 2) {
+          // float form: RZ(u * 512 r + tab0 + 256) = tab0 + (k - idx) * 512 + 9 fraction bits
+          const float r9 = __int_as_float(gpar.y) * 512.0f;
+          const int32_t nlo = gpar.x - gmax;
+#pragma unroll
+          for (int q = 0; q < 2; ++q) {
+            uint32_t pw[4];
+#pragma unroll
+            for (int e = 0; e < 4; e += 2) {
+              uint32_t u0 = (uint32_t)__viaddmax_s32((int32_t)v8[4 * q + e], nlo, 0);
+              uint32_t u1 = (uint32_t)__viaddmax_s32((int32_t)v8[4 * q + e + 1], nlo, 0);
+              if (!open) {
+                u0 = ((bits >> (4 * q + e)) & 1u) ? 0u : u0;
+                u1 = ((bits >> (4 * q + e + 1)) & 1u) ? 0u : u1;
+              }
+              float f0, f1;
+              fma_rz_f32x2(f0, f1, __uint_as_float(u0), __uint_as_float(u1), r9, tabden);
+              pw[e] = lds_u32(and_or(__float_as_uint(f0), 0xFFFFFE00u, row4));
+              pw[e + 1] = lds_u32(and_or(__float_as_uint(f1), 0xFFFFFE00u, row4));
+            }
+            pk[2 * c + q] = __byte_perm(__byte_perm(pw[0], pw[1], 0x0040),
+                                        __byte_perm(pw[2], pw[3], 0x0040), 0x5410);
+          }
+          continue;
+        }
+        GkMap gmap;
+        gmap.init(gmax, gpar, k);
         if (open && gmap.use32) {
 #pragma unroll
           for (int q = 0; q < 2; ++q) {
-            const uint32_t p0 = lds_u32(tab_row + (gmap.idx32((int32_t)v8[4 * q], nk2) << 9));
-            const uint32_t p1 = lds_u32(tab_row + (gmap.idx32((int32_t)v8[4 * q + 1], nk2) << 9));
-            const uint32_t p2 = lds_u32(tab_row + (gmap.idx32((int32_t)v8[4 * q + 2], nk2) << 9));
-            const uint32_t p3 = lds_u32(tab_row + (gmap.idx32((int32_t)v8[4 * q + 3], nk2) << 9));
+            const uint32_t p0 = lds_u32(tab_row + ((k - gmap.idx32((int32_t)v8[4 * q], nk2)) << 9));
+            const uint32_t p1 = lds_u32(tab_row + ((k - gmap.idx32((int32_t)v8[4 * q + 1], nk2)) << 9));
+            const uint32_t p2 = lds_u32(tab_row + ((k - gmap.idx32((int32_t)v8[4 * q + 2], nk2)) << 9));
+            const uint32_t p3 = lds_u32(tab_row + ((k - gmap.idx32((int32_t)v8[4 * q + 3], nk2)) << 9));
             pk[2 * c + q] = __byte_perm(__byte_perm(p0, p1, 0x0040), __byte_perm(p2, p3, 0x0040), 0x5410);
           }
         } else {
 #pragma unroll
           for (int e = 0; e < 8; ++e)
             if (!((bits >> e) & 1u))
-              pk[2 * c + (e >> 2)] |= lds_u32(tab_row + (gmap.idx((int32_t)v8[e], nk2, k) << 9))
+              pk[2 * c + (e >> 2)] |= lds_u32(tab_row + ((k - gmap.idx((int32_t)v8[e], nk2, k)) << 9))
                                       << (8 * (e & 3));
         }
       }
@@ -863,7 +925,7 @@ __global__ void __launch_bounds__(Cfg<DP>::NTHREADS, 1)
     const bool trw = IA_PROFILE && lane == 0;  // one trace segment per softmax warp
     if (tm) IA_TMARK(0);
     if constexpr (GK) {
-      gk_passes<DP, DEBUG>(p, smem, reinterpret_cast<uint32_t*>(tab), xsum, lut8, s_full, s_free,
+      gk_passes<DP, DEBUG>(p, smem, reinterpret_cast<uint32_t*>(tab), xsum, lut8, lut8r, s_full, s_free,
                            p_full, p_free, s_base, wg, row, lane, i, lim, bh, n_kt, row_valid,
                            resident, s_ph);
     } else {

@@ -89,6 +89,12 @@ __global__ void group_params_kernel(const float* __restrict__ qs, const float* _
     gp.magic = hp.magic;
     gp.shift = hp.shift;
     gp.use32 = hp.use32;
+    // float form of the index map (params.cuh): the fused kernel then needs only c_eff and
+    // the ratio, whose bits travel in `magic`
+    if (float_idx_ok(hp.c_eff, (int64_t)nlut - 1)) {
+      gp.magic = __float_as_uint(float_idx_ratio(hp.c_eff, (int64_t)nlut - 1));
+      gp.use32 = hp.use32 | 2;
+    }
   }
   out[u] = gp;
 }
