@@ -68,6 +68,25 @@ def test_grouped_fused_int_attention_api_matches_reference_fixtures():
             assert t.qk_gemm_ns == 0 and t.pv_gemm_ns == 0
 
 
+@pytest.mark.parametrize("scale", [0.25, 0.05, 0.004])
+@pytest.mark.parametrize("masked", [False, True])
+def test_grouped_fused_integer_form_groups(scale, masked):
+    """Small operand scales make c_int large: groups whose c_eff (2k + 1) >= 2^23 leave the
+    float index form for the magic-number form (and, smaller still, the c_eff sentinel);
+    with per-row K magnitudes spread over 20x the two forms mix inside one head, sharing
+    the reversed row table."""
+    L, d, gs = 576, 64, 16
+    q, k, v = _inputs(1, 2, 1, L, d, seed=21)
+    q *= np.float32(scale)
+    k *= np.float32(scale)
+    mask = None
+    if masked:
+        mask = np.random.default_rng(9).random((L, L)) < 0.25
+    got = ia.int_attention_batched(q, k, v, causal=not masked, mask=mask, k_group_size=gs)
+    want = O.attention_grouped_batched(q, k, v, gs, causal=not masked, mask=mask)
+    assert np.array_equal(got.view(np.uint32), want.view(np.uint32))
+
+
 def test_grouped_fused_c3_shape():
     """C3-shaped (L = 2048, d = 128, causal) with 64-key K groups, 4 heads."""
     q, k, v = _inputs(1, 4, 2, 2048, 128, seed=3)
