@@ -44,6 +44,11 @@
 #include "params.cuh"
 #include "ptx.cuh"
 
+// epilogue staging with 16-byte shared-memory accesses (conflict-free pitch)
+#ifndef IA_STAGE_V4
+#define IA_STAGE_V4 1
+#endif
+
 namespace ia {
 
 constexpr int BM = 128;  // query rows per tile (= TMEM lanes)
@@ -111,7 +116,11 @@ struct Cfg {
   __host__ __device__ static constexpr int k_off(int s) {
     return s < NKST ? OFF_K + s * K_BYTES : OFF_P + (s - NKST) * K_BYTES;
   }
-  static constexpr int STAGE_PITCH = DP + 1;  // f32 epilogue staging row pitch (words, conflict-free)
+  // f32 epilogue staging row pitch (words): 16-byte aligned rows, and 8 consecutive rows'
+  // 16-byte units fall in 8 different bank groups (33 r mod 8), so both the per-row STS.128
+  // of the writers and the LDS.128 of the coalescing readers are conflict-free (the former
+  // DP + 1 pitch made every scalar read-back 4-way conflicted: 8 K wavefronts per CTA)
+  static constexpr int STAGE_PITCH = IA_STAGE_V4 ? DP + 4 : DP + 1;
   static_assert(OFF_TAB >= BM * STAGE_PITCH * 4, "epilogue staging must fit in Q/K/V stages");
   static_assert(OFF_TAB % 512 == 0, "row-table base: idx * 512 is OR-ed into the address");
 };
@@ -1473,10 +1482,22 @@ __global__ void __launch_bounds__(Cfg<DP>::NTHREADS, 1)
     for (int c0 = wg * 16; c0 < DP; c0 += 16 * NWG) {
       uint32_t a[16];
       tmem_ld16(tmem + t_lane + C::O_COL + c0, a);
+      if (IA_STAGE_V4) {
+#pragma unroll
+        for (int e = 0; e < 16; e += 4) {
+          float4 f;
+          f.x = row_valid ? __fmul_rn(__int2float_rn((int32_t)a[e]), osc) : 0.0f;
+          f.y = row_valid ? __fmul_rn(__int2float_rn((int32_t)a[e + 1]), osc) : 0.0f;
+          f.z = row_valid ? __fmul_rn(__int2float_rn((int32_t)a[e + 2]), osc) : 0.0f;
+          f.w = row_valid ? __fmul_rn(__int2float_rn((int32_t)a[e + 3]), osc) : 0.0f;
+          *reinterpret_cast<float4*>(stage + row * C::STAGE_PITCH + c0 + e) = f;
+        }
+      } else {
 #pragma unroll
       for (int e = 0; e < 16; ++e)
         stage[row * C::STAGE_PITCH + c0 + e] =
             row_valid ? __fmul_rn(__int2float_rn((int32_t)a[e]), osc) : 0.0f;
+      }
       if (DEBUG && p.dbg_acc && i < p.L) {
         for (int e = 0; e < 16; ++e)
           p.dbg_acc[((size_t)bh * p.L + i) * DP + c0 + e] = (int32_t)a[e];
@@ -1492,14 +1513,16 @@ __global__ void __launch_bounds__(Cfg<DP>::NTHREADS, 1)
       for (int t = tid; t < rows * D4; t += NWT) {
         const int r = t / D4, c4 = (t % D4) * 4;
         const float* s4 = stage + r * C::STAGE_PITCH + c4;
-        *reinterpret_cast<float4*>(obase + (size_t)r * DP + c4) = make_float4(s4[0], s4[1], s4[2], s4[3]);
+        *reinterpret_cast<float4*>(obase + (size_t)r * DP + c4) =
+            IA_STAGE_V4 ? *reinterpret_cast<const float4*>(s4) : make_float4(s4[0], s4[1], s4[2], s4[3]);
       }
     } else if ((p.d & 3) == 0) {
       const int d4 = p.d >> 2;
       for (int t = tid; t < rows * d4; t += NWT) {
         const int r = t / d4, c4 = (t - r * d4) << 2;
         const float* s4 = stage + r * C::STAGE_PITCH + c4;
-        *reinterpret_cast<float4*>(obase + (size_t)r * p.d + c4) = make_float4(s4[0], s4[1], s4[2], s4[3]);
+        *reinterpret_cast<float4*>(obase + (size_t)r * p.d + c4) =
+            IA_STAGE_V4 ? *reinterpret_cast<const float4*>(s4) : make_float4(s4[0], s4[1], s4[2], s4[3]);
       }
     } else {
       for (int t = tid; t < rows * p.d; t += NWT) {
