@@ -8,8 +8,10 @@
 // does not use it -- it is the unfused / per-stage path.
 //
 // One CTA per 128x128 output tile; K streamed in 128-byte (SWIZZLE_128B)
-// blocks through a 4-stage TMA ring; warp 0 = TMA, warp 1 = MMA issuer,
-// warp 2 = TMEM allocator, warps 4-7 = epilogue (TMEM -> registers -> global).
+// blocks through a 3-stage TMA ring (97 KB: two CTAs per SM, so one CTA's epilogue
+// overlaps the other's main loop); warp 0 = TMA, warp 1 = MMA issuer, warp 2 = TMEM
+// allocator (128 columns), warps 4-7 = epilogue (TMEM -> registers -> 16-byte global
+// stores, each thread filling whole 128-byte lines of its row).
 #include <cstdint>
 
 #include "common.cuh"
@@ -20,10 +22,10 @@ namespace ia {
 int make_tmap_2d_u8(CUtensorMap* m, const void* base, uint64_t d0, uint64_t d1, uint64_t stride1,
                     uint32_t b0, uint32_t b1, int swizzle_bytes);
 
-constexpr int G_BM = 128, G_BN = 128, G_BK = 128, G_ST = 4, G_THREADS = 256;
+constexpr int G_BM = 128, G_BN = 128, G_BK = 128, G_ST = 3, G_THREADS = 256;
 constexpr int G_TILE = G_BM * G_BK;  // bytes per A (or B) stage
 
-__global__ void __launch_bounds__(G_THREADS, 1)
+__global__ void __launch_bounds__(G_THREADS, 2)
     gemm_i8_kernel(const __grid_constant__ CUtensorMap tma, const __grid_constant__ CUtensorMap tmb,
                    int32_t* __restrict__ C, int64_t ldc, int M, int N, int K, uint32_t idesc) {
   extern __shared__ uint8_t smem_raw[];
@@ -83,6 +85,7 @@ __global__ void __launch_bounds__(G_THREADS, 1)
   } else if (warp >= 4) {
     const int quad = warp & 3;
     const int r = m0 + quad * 32 + lane;
+    const bool vec_ok = ((ldc & 3) == 0) && ((reinterpret_cast<uintptr_t>(C) & 15) == 0);
     mbar_wait(done, 0);
     tc_fence_after();
 #pragma unroll 1
@@ -91,9 +94,16 @@ __global__ void __launch_bounds__(G_THREADS, 1)
       tmem_ld32(tmem + ((uint32_t)(quad * 32) << 16) + c, v);
       if (r < M) {
         int32_t* crow = C + (int64_t)r * ldc + n0 + c;
+        if (vec_ok && n0 + c + 32 <= N) {  // whole 128-byte line of this row
 #pragma unroll
-        for (int e = 0; e < 32; ++e)
-          if (n0 + c + e < N) crow[e] = (int32_t)v[e];
+          for (int e = 0; e < 32; e += 4)
+            *reinterpret_cast<int4*>(crow + e) =
+                make_int4((int)v[e], (int)v[e + 1], (int)v[e + 2], (int)v[e + 3]);
+        } else {
+#pragma unroll
+          for (int e = 0; e < 32; ++e)
+            if (n0 + c + e < N) crow[e] = (int32_t)v[e];
+        }
       }
     }
   }
