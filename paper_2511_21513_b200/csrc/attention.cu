@@ -264,6 +264,10 @@ __device__ __forceinline__ void bwait(uint64_t* bar, uint32_t parity, bool spin)
 #define IA_UNIFORM_WARP 0
 #endif
 // rows of at least this many key tiles use the pass-3 group skip
+// grouped K: batch-level fast path (float form, unmasked) and pass-B chunk skip
+#ifndef IA_GK_FAST
+#define IA_GK_FAST 1
+#endif
 #ifndef IA_SKIP_MIN_KT
 #define IA_SKIP_MIN_KT 16
 #endif
@@ -351,6 +355,47 @@ __device__ __forceinline__ void gk_group_max(const AttnDev& p, uint32_t s_tile, 
   }
 }
 
+// The same for one 64-key batch already in registers (groups of <= 64 keys never straddle
+// a batch, so their maxima need no second TMEM read): gm8[c] for the batch's 8 chunks.
+__device__ __forceinline__ void gk_batch_max(const AttnDev& p, const uint32_t (&va)[32],
+                                             const uint32_t (&vb)[32], uint32_t ma, uint32_t mb,
+                                             bool open, int32_t* gm8) {
+  if (open) {
+#pragma unroll
+    for (int c = 0; c < 8; ++c) {
+      const uint32_t* v8 = c < 4 ? &va[8 * c] : &vb[8 * (c - 4)];
+      int32_t x = __vimax3_s32((int32_t)v8[0], (int32_t)v8[1], (int32_t)v8[2]);
+      x = __vimax3_s32(x, (int32_t)v8[3], (int32_t)v8[4]);
+      x = __vimax3_s32(x, (int32_t)v8[5], (int32_t)v8[6]);
+      gm8[c] = max(x, (int32_t)v8[7]);
+    }
+  } else {
+#pragma unroll
+    for (int c = 0; c < 8; ++c) {
+      const uint32_t* v8 = c < 4 ? &va[8 * c] : &vb[8 * (c - 4)];
+      const uint32_t bits = ((c < 4 ? ma : mb) >> (8 * (c & 3))) & 0xffu;
+      int32_t x = INT_MIN;
+#pragma unroll
+      for (int e = 0; e < 8; ++e)
+        if (!((bits >> e) & 1u)) x = max(x, (int32_t)v8[e]);
+      gm8[c] = x;
+    }
+  }
+  const int gs8 = 1 << (p.gs_log2 - 3);
+#pragma unroll
+  for (int s = 1; s < 8; s <<= 1) {
+    if (gs8 > s) {
+#pragma unroll
+      for (int c = 0; c < 8; ++c)
+        if (!(c & s)) {
+          const int32_t t = max(gm8[c], gm8[c | s]);
+          gm8[c] = t;
+          gm8[c | s] = t;
+        }
+    }
+  }
+}
+
 // idx of logit a in a group with row max m (softmax.py:380-386 with the group's c).
 struct GkMap {
   int32_t lo;
@@ -402,7 +447,8 @@ __device__ __forceinline__ void gk_passes(const AttnDev& p, uint8_t* smem, uint3
     s_ph ^= 1u;
     tc_fence_after();
     int32_t gm[16];
-    gk_group_max(p, s_base, row_valid, i, n * BN, lim, gm);
+    const bool two_reads = p.gs_log2 == 7;  // 128-key groups span both batches of the tile
+    if (two_reads) gk_group_max(p, s_base, row_valid, i, n * BN, lim, gm);
 #pragma unroll 1
     for (int hb = 0; hb < 2; ++hb) {
       uint32_t va[32], vb[32];
@@ -416,9 +462,47 @@ __device__ __forceinline__ void gk_passes(const AttnDev& p, uint8_t* smem, uint3
       const uint32_t ma = gk_mask32(p, row_valid, i, j0, lim);
       const uint32_t mb = gk_mask32(p, row_valid, i, j0 + 32, lim);
       const bool open = !__any_sync(0xffffffffu, (ma | mb) != 0u);  // no key masked in the warp
+      int32_t gb[8];  // this batch's group maxima per 8-key chunk
+      if (two_reads) {
+#pragma unroll
+        for (int c = 0; c < 8; ++c) gb[c] = hb ? gm[8 + c] : gm[c];
+      } else {
+        gk_batch_max(p, va, vb, ma, mb, open, gb);
+      }
+      if (IA_GK_FAST && open) {
+        // Batch-level fast path: no key masked and every group of these 64 keys in the float
+        // form (warp-uniform) -- straight-line code over the batch, the eight chunks'
+        // parameters loaded up front.
+        int32_t gcx[8], gry[8];  // c_eff and the f32 ratio bits of each chunk's group
+        int allf = 2;
+#pragma unroll
+        for (int c = 0; c < 8; ++c) {
+          const int4 g4 = __ldg(gp + ((j0 + 8 * c) >> p.gs_log2));
+          gcx[c] = g4.x;
+          gry[c] = g4.y;
+          allf &= g4.w;
+        }
+        if (allf) {
+#pragma unroll
+          for (int c = 0; c < 8; ++c) {
+            const uint32_t* v8 = c < 4 ? &va[8 * c] : &vb[8 * (c - 4)];
+            const float rg = __int_as_float(gry[c]);
+            const int32_t nlo = gcx[c] - gb[c];
+#pragma unroll
+            for (int e = 0; e < 8; e += 2) {
+              const uint32_t u0 = (uint32_t)__viaddmax_s32((int32_t)v8[e], nlo, 0);
+              const uint32_t u1 = (uint32_t)__viaddmax_s32((int32_t)v8[e + 1], nlo, 0);
+              float f0, f1;
+              fma_rn_f32x2(f0, f1, __uint_as_float(u0), __uint_as_float(u1), rg, lutden);
+              S += lds_u8(__float_as_uint(f0)) + lds_u8(__float_as_uint(f1));
+            }
+          }
+          continue;
+        }
+      }
 #pragma unroll
       for (int c = 0; c < 8; ++c) {
-        const int32_t gmax = hb ? gm[8 + c] : gm[c];
+        const int32_t gmax = gb[c];
         if (gmax == INT_MIN) continue;  // every key of the chunk is masked: e = 0
         const int4 gpar = __ldg(gp + ((j0 + 8 * c) >> p.gs_log2));
         const uint32_t* v8 = c < 4 ? &va[8 * c] : &vb[8 * (c - 4)];
@@ -480,6 +564,18 @@ __device__ __forceinline__ void gk_passes(const AttnDev& p, uint8_t* smem, uint3
   }
   named_bar_sync(1, NWT);
 
+  // Pass-B skip threshold in the index domain: P^ = rowtab[idx] > 0 only for idx <= t*
+  // (t* = the largest t with 2 scale lut[t] >= S, every entry scanned), i.e. only for
+  // j = k - idx >= jmin = k - t*; j is monotone in u = a - lo_g, so a chunk whose largest
+  // logit maps below jmin in every row of the warp is all zero.  Rows of >= 16 key tiles.
+  uint32_t jmin = 0u;  // 0: no chunk is skipped
+  if (IA_GK_FAST && n_kt >= IA_SKIP_MIN_KT) {
+    int tstar = -1;
+    if (row_valid && S)
+      for (int t = 0; t < nlut; ++t)
+        if ((uint32_t)p.scale_x2 * (uint32_t)lut8[t] >= S) tstar = t;
+    jmin = tstar < 0 ? k + 1u : k - (uint32_t)tstar;  // no nonzero entry: nothing is live
+  }
   // ---- pass B: P^ = rowtab[idx_g] -> smem -> P.V MMA
   const uint32_t tab_row = smem_u32(tab) + (uint32_t)row * 4u;
   const uint32_t row4 = (uint32_t)row * 4u;
@@ -497,7 +593,8 @@ __device__ __forceinline__ void gk_passes(const AttnDev& p, uint8_t* smem, uint3
     const uint32_t p_row = p_rows + (uint32_t)(pbl * C::P_BYTES);
     mbar_wait(p_free + wg * C::NPB + pbl, ((uint32_t)(tl / C::NPB) & 1u) ^ 1u);
     int32_t gm[16];
-    gk_group_max(p, s_base, row_valid, i, n * BN, lim, gm);
+    const bool two_reads = p.gs_log2 == 7;
+    if (two_reads) gk_group_max(p, s_base, row_valid, i, n * BN, lim, gm);
 #pragma unroll 1
     for (int hb = 0; hb < 2; ++hb) {
       uint32_t va[32], vb[32];
@@ -514,9 +611,72 @@ __device__ __forceinline__ void gk_passes(const AttnDev& p, uint8_t* smem, uint3
 #pragma unroll
       for (int q = 0; q < 16; ++q) pk[q] = 0u;
       const bool open = !__any_sync(0xffffffffu, (ma | mb) != 0u);
+      int32_t gb[8];  // this batch's group maxima per 8-key chunk
+      if (two_reads) {
+#pragma unroll
+        for (int c = 0; c < 8; ++c) gb[c] = hb ? gm[8 + c] : gm[c];
+      } else {
+        gk_batch_max(p, va, vb, ma, mb, open, gb);
+      }
+      bool fast_done = false;
+      if (IA_GK_FAST && open) {
+        int32_t gcx[8], gry[8];  // c_eff and the f32 ratio bits of each chunk's group
+        int allf = 2;
+#pragma unroll
+        for (int c = 0; c < 8; ++c) {
+          const int4 g4 = __ldg(gp + ((j0 + 8 * c) >> p.gs_log2));
+          gcx[c] = g4.x;
+          gry[c] = g4.y;
+          allf &= g4.w;
+        }
+        if (allf) {
+          // live chunks: the chunk's largest logit reaches an index with a nonzero table
+          // entry in some row of the warp (all eight decisions at once, one REDUX.OR)
+          uint32_t live = 0xffu;
+          if (n_kt >= IA_SKIP_MIN_KT) {
+            uint32_t lm = 0u;
+#pragma unroll
+            for (int c = 0; c < 8; ++c) {
+              const uint32_t* v8 = c < 4 ? &va[8 * c] : &vb[8 * (c - 4)];
+              int32_t cm = __vimax3_s32((int32_t)v8[0], (int32_t)v8[1], (int32_t)v8[2]);
+              cm = __vimax3_s32(cm, (int32_t)v8[3], (int32_t)v8[4]);
+              cm = __vimax3_s32(cm, (int32_t)v8[5], (int32_t)v8[6]);
+              const int32_t nlo = gcx[c] - gb[c];
+              const uint32_t um = (uint32_t)__viaddmax_s32(max(cm, (int32_t)v8[7]), nlo, 0);
+              const float fj = __fmaf_rn(__uint_as_float(um), __int_as_float(gry[c]), 0.0f);
+              lm |= __float_as_uint(fj) >= jmin ? (1u << c) : 0u;
+            }
+            live = __reduce_or_sync(0xffffffffu, lm);
+          }
+#pragma unroll
+          for (int c = 0; c < 8; ++c) {
+            if (!((live >> c) & 1u)) continue;  // pk stays 0
+            const uint32_t* v8 = c < 4 ? &va[8 * c] : &vb[8 * (c - 4)];
+            const float r9 = __int_as_float(gry[c]) * 512.0f;
+            const int32_t nlo = gcx[c] - gb[c];
+#pragma unroll
+            for (int q = 0; q < 2; ++q) {
+              uint32_t pw[4];
+#pragma unroll
+              for (int e = 0; e < 4; e += 2) {
+                const uint32_t u0 = (uint32_t)__viaddmax_s32((int32_t)v8[4 * q + e], nlo, 0);
+                const uint32_t u1 = (uint32_t)__viaddmax_s32((int32_t)v8[4 * q + e + 1], nlo, 0);
+                float f0, f1;
+                fma_rz_f32x2(f0, f1, __uint_as_float(u0), __uint_as_float(u1), r9, tabden);
+                pw[e] = lds_u32(and_or(__float_as_uint(f0), 0xFFFFFE00u, row4));
+                pw[e + 1] = lds_u32(and_or(__float_as_uint(f1), 0xFFFFFE00u, row4));
+              }
+              pk[2 * c + q] = __byte_perm(__byte_perm(pw[0], pw[1], 0x0040),
+                                          __byte_perm(pw[2], pw[3], 0x0040), 0x5410);
+            }
+          }
+          fast_done = true;
+        }
+      }
 #pragma unroll
       for (int c = 0; c < 8; ++c) {
-        const int32_t gmax = hb ? gm[8 + c] : gm[c];
+        if (fast_done) break;
+        const int32_t gmax = gb[c];
         if (gmax == INT_MIN) continue;
         const int4 gpar = __ldg(gp + ((j0 + 8 * c) >> p.gs_log2));
         const uint32_t* v8 = c < 4 ? &va[8 * c] : &vb[8 * (c - 4)];
