@@ -817,23 +817,21 @@ __global__ void __launch_bounds__(Cfg<DP>::NTHREADS, 1)
   constexpr int PV_PASS = (QO || GK) ? 1 : 2;  // tile t >= PV_PASS * n_kt: the P / P.V pass
   const int n_kt_b = (XF(1)) ? 0 : n_kt;  // key tiles of passes 2-3 / P.V
 
-  if (rw == 0 && lane == 0) {
-    prefetch_tmap(&tmq);
-    prefetch_tmap(&tmk);
-    prefetch_tmap(&tmv);
-    mbar_init(q_full, 1);
-    for (int s = 0; s < C::NKX; ++s) { mbar_init(k_full + s, 1); mbar_init(k_empty + s, 1); }
-    for (int s = 0; s < C::NVST; ++s) { mbar_init(v_full + s, 1); mbar_init(v_empty + s, 1); }
-    for (int w = 0; w < NWG; ++w) {
-      mbar_init(s_full + w, 1);
-      mbar_init(s_free + w, 4);  // one arrive per warp of the warpgroup
+  if (rw == 0) {
+    if (lane == 0) {
+      prefetch_tmap(&tmq);
+      prefetch_tmap(&tmk);
+      prefetch_tmap(&tmv);
     }
-    for (int w = 0; w < NWG * C::NPB; ++w) {
-      mbar_init(p_full + w, 4);
-      mbar_init(p_free + w, 1);
-    }
-    mbar_init(o_full, 1);
+    // the barriers are one contiguous array: each lane initialises its share (a fixed cost
+    // of every CTA, ~40 serial mbarrier.init otherwise).  s_free and p_full take one arrive
+    // per warp of a warpgroup, every other barrier one.
+    constexpr int NB = 1 + 2 * C::NKX + 2 * C::NVST + 2 * NWG + 2 * NWG * C::NPB + 1;
+    constexpr int I4_LO = 1 + 2 * C::NKX + 2 * C::NVST + NWG;  // s_free[0]
+    constexpr int I4_HI = I4_LO + NWG + NWG * C::NPB;          // p_free[0]
+    for (int bi = lane; bi < NB; bi += 32) mbar_init(bars + bi, (bi >= I4_LO && bi < I4_HI) ? 4 : 1);
     fence_mbar_init();
+    __syncwarp();
   }
   if (rw == 2) {
     tmem_alloc(tmem_slot, TMEM_COLS);
