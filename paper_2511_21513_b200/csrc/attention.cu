@@ -173,6 +173,9 @@ __device__ __forceinline__ uint32_t and_or(uint32_t a, uint32_t b, uint32_t c) {
   asm("lop3.b32 %0, %1, %2, %3, 0xEA;" : "=r"(r) : "r"(a), "r"(b), "r"(c));  // (a & b) | c
   return r;
 }
+__device__ __forceinline__ void sts_u32(uint32_t addr, uint32_t v) {
+  asm volatile("st.shared.u32 [%0], %1;" ::"r"(addr), "r"(v) : "memory");
+}
 __device__ __forceinline__ uint32_t lds_u32(uint32_t addr) {
   uint32_t v;
   asm("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(addr));
@@ -1365,20 +1368,37 @@ __global__ void __launch_bounds__(Cfg<DP>::NTHREADS, 1)
       // zero-extension of the integer form's table is not built (short rows: the table
       // build is a fixed cost per CTA)
       const int nbuild = flc ? nlut : ntab;
-      for (int t = wg; t < nbuild; t += NWG) {  // lut8[t] = 0 (incl. t >= nlut) -> S / 2S = 0
-        const uint32_t lt = lut8[t];
-        uint32_t pv = 0u;
-        if (S && lt) {
-          const uint32_t num = (uint32_t)p.scale_x2 * lt + S;
+      // Branch-free, shared-window addressing (a fixed cost of every CTA: ~11 entries per
+      // thread).  lt = 0 (a zero LUT entry, t >= nlut, or S = 0) gives num = S, q = 0.
+      const uint32_t lut_s = smem_u32(lut8), tab_s = smem_u32(tab);
+      const uint32_t sx2 = (uint32_t)p.scale_x2;
+      const int kk = (int)k;
+      if (wtab) {
+        // entry address: (tt * 128 + row) * 4; float form: tt = k - t for t <= k
+        const uint32_t a_row = tab_s + (uint32_t)row * 4u;
+#pragma unroll 4
+        for (int t = wg; t < nbuild; t += NWG) {
+          const uint32_t lt = S ? lds_u8(lut_s + (uint32_t)t) : 0u;
+          const uint32_t num = sx2 * lt + S;
           int32_t q = __float2int_rz(__fmul_rn((float)num, rden));
           const int32_t r = (int32_t)num - q * (int32_t)two_s;
           q += r < 0 ? -1 : (r >= (int32_t)two_s ? 1 : 0);
-          pv = (uint32_t)q;
+          const int tt = (flc && t <= kk) ? kk - t : t;
+          sts_u32(a_row + ((uint32_t)tt << 9), S ? (uint32_t)q : 0u);
         }
-        // float form: entry j = k - t (entries past k are never addressed: u <= c_eff)
-        const int tt = flc ? (t <= (int)k ? (int)k - t : t) : t;
-        if (wtab) reinterpret_cast<uint32_t*>(tab)[tt * 128 + row] = pv;
-        else tab[tt * 128 + row] = (uint8_t)pv;
+      } else {
+        for (int t = wg; t < nbuild; t += NWG) {
+          const uint32_t lt = lut8[t];
+          uint32_t pv = 0u;
+          if (S && lt) {
+            const uint32_t num = sx2 * lt + S;
+            int32_t q = __float2int_rz(__fmul_rn((float)num, rden));
+            const int32_t r = (int32_t)num - q * (int32_t)two_s;
+            q += r < 0 ? -1 : (r >= (int32_t)two_s ? 1 : 0);
+            pv = (uint32_t)q;
+          }
+          tab[t * 128 + row] = (uint8_t)pv;
+        }
       }
     }
     named_bar_sync(1, NWT);
