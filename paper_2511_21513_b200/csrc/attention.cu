@@ -271,6 +271,10 @@ __device__ __forceinline__ void bwait(uint64_t* bar, uint32_t parity, bool spin)
 #ifndef IA_GK_FAST
 #define IA_GK_FAST 1
 #endif
+// pass 1 (MMA-bound, light softmax work): poll s_full instead of the suspended wait
+#ifndef IA_P1_SPIN
+#define IA_P1_SPIN 0
+#endif
 #ifndef IA_SKIP_MIN_KT
 #define IA_SKIP_MIN_KT 16
 #endif
@@ -1115,7 +1119,7 @@ __global__ void __launch_bounds__(Cfg<DP>::NTHREADS, 1)
     float qm = -INFINITY, qs = 0.0f;
     for (int n = wg; n < n_kt; n += NWG) {
       long long tw0 = clk64();
-      bwait(s_full + wg, s_ph, XF(4));
+      bwait(s_full + wg, s_ph, IA_P1_SPIN || XF(4));
       if (trw) IA_TRACE(4 + sw, 8, 0 * n_kt + n);
       s_ph ^= 1u;
       if (tm) IA_TADD(15, clk64() - tw0);
