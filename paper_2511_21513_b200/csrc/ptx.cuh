@@ -2,6 +2,7 @@
 // Hand-written for this library (no CUTLASS/CuTe dependency).
 #pragma once
 #include <cstdint>
+#include <cstdio>
 #include <cuda.h>
 #include <cuda_runtime.h>
 
@@ -63,6 +64,13 @@ __device__ __forceinline__ uint32_t mbar_try_wait(uint32_t bar, uint32_t parity)
 #ifndef IA_WAIT_STYLE
 #define IA_WAIT_STYLE 0
 #endif
+// watchdog period (log2 SM cycles); debug builds shorten it and print the stuck waiter
+#ifndef IA_WATCHDOG_LOG2
+#define IA_WATCHDOG_LOG2 36
+#endif
+#ifndef IA_WATCHDOG_PRINT
+#define IA_WATCHDOG_PRINT 0
+#endif
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   const uint32_t a = smem_u32(bar);
   if (mbar_try_wait(a, parity)) return;
@@ -73,12 +81,18 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
 #pragma unroll
     for (int i = 0; i < 8; ++i)
       if (mbar_try_wait(a, parity)) return;
-    if (clock64() - t0 > (1ll << 36)) __trap();
+    if (clock64() - t0 > (1ll << IA_WATCHDOG_LOG2)) __trap();
   }
 #else
   uint32_t spins = 0;
   while (!mbar_try_wait(a, parity)) {
-    if ((++spins & 1023u) == 0 && clock64() - t0 > (1ll << 36)) __trap();
+    if ((++spins & 1023u) == 0 && clock64() - t0 > (1ll << IA_WATCHDOG_LOG2)) {
+#if IA_WATCHDOG_PRINT
+      printf("watchdog: block %d thread %d barrier smem 0x%x parity %u\n", (int)blockIdx.x,
+             (int)threadIdx.x, a, parity);
+#endif
+      __trap();
+    }
   }
 #endif
 }
@@ -118,7 +132,7 @@ __device__ __forceinline__ void mbar_wait_backoff(uint64_t* bar, uint32_t parity
   const long long t0 = clock64();
   do {
     __nanosleep(ns);
-    if (clock64() - t0 > (1ll << 36)) __trap();
+    if (clock64() - t0 > (1ll << IA_WATCHDOG_LOG2)) __trap();
   } while (!mbar_test(bar, parity));
 }
 __device__ __forceinline__ void mbar_wait_spin(uint64_t* bar, uint32_t parity) {
@@ -126,7 +140,7 @@ __device__ __forceinline__ void mbar_wait_spin(uint64_t* bar, uint32_t parity) {
   const long long t0 = clock64();
   uint32_t spins = 0;
   while (!mbar_poll(a, parity)) {
-    if ((++spins & 1023u) == 0 && clock64() - t0 > (1ll << 36)) __trap();
+    if ((++spins & 1023u) == 0 && clock64() - t0 > (1ll << IA_WATCHDOG_LOG2)) __trap();
   }
 }
 
