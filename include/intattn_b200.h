@@ -232,6 +232,11 @@ int ia_gemm_i8(const void* A, int64_t lda, int a_signed, const int8_t* B, int64_
 int ia_copy_rows_async(void* dst, int64_t dpitch, const void* src, int64_t spitch,
                        int64_t width, int64_t height, void* stream);
 
+/* Zeroes `bytes` bytes of device scratch on the stream (cudaMemsetAsync): the quantiser's
+ * amax slots, team arrival counters and error flag must be zero before each call, and a
+ * memset node costs no kernel launch of the caller's framework. */
+int ia_zero_async(void* dst, int64_t bytes, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

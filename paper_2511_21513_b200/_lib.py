@@ -33,7 +33,7 @@ EXPORTS = (
     "ia_quant_amax_rows", "ia_quant_amax_cols", "ia_quant_scales", "ia_quantize",
     "ia_dequantize", "ia_quant_heads", "ia_quant_tensors", "ia_head_params_host", "ia_softmax_params_host", "ia_head_params_dev",
     "ia_mask_pack", "ia_attn_fwd", "ia_attn_supported", "ia_index_softmax", "ia_index_softmax_grouped",
-    "ia_gemm_i8", "ia_copy_rows_async", "ia_group_params_dev",
+    "ia_gemm_i8", "ia_copy_rows_async", "ia_group_params_dev", "ia_zero_async",
 )
 
 
@@ -120,6 +120,7 @@ def load():
             "ia_copy_rows_async": ([P, i64, P, i64, i64, i64, P], i32),
             "ia_group_params_dev": ([P, P, i64, i64, i64, i64, i64, ctypes.c_double, i32, P, P],
                                     i32),
+            "ia_zero_async": ([P, i64, P], i32),
         }
         for name, (args, res) in sig.items():
             fn = getattr(L, name)

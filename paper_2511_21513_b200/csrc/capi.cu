@@ -213,3 +213,11 @@ extern "C" int ia_copy_rows_async(void* dst, int64_t dpitch, const void* src, in
   if (e != cudaSuccess) return fail(IA_ERR_CUDA, "ia_copy_rows_async: %s", cudaGetErrorString(e));
   return IA_OK;
 }
+
+extern "C" int ia_zero_async(void* dst, int64_t bytes, void* stream) {
+  if (!dst || bytes < 0) return fail(IA_ERR_INVALID_ARGUMENT, "ia_zero_async: bad arguments");
+  if (!bytes) return IA_OK;
+  cudaError_t e = cudaMemsetAsync(dst, 0, (size_t)bytes, (cudaStream_t)stream);
+  if (e != cudaSuccess) return fail(IA_ERR_CUDA, "ia_zero_async: %s", cudaGetErrorString(e));
+  return IA_OK;
+}

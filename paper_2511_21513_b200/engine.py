@@ -71,7 +71,10 @@ class Workspace:
     + the non-finite flag."""
 
     def __init__(self, n_slots: int, device):
-        self.buf = torch.zeros(2 * n_slots + 1, dtype=torch.int32, device=device)
+        # zeroed by a memset node of the library (no framework fill kernel per call)
+        self.buf = torch.empty(2 * n_slots + 1, dtype=torch.int32, device=device)
+        _lib.check(_lib.load().ia_zero_async(_p(self.buf), self.buf.numel() * 4, _stream()),
+                   "workspace zero")
         self.amax = self.buf[:n_slots]
         self.count = self.buf[n_slots:2 * n_slots]
         self.err = self.buf[2 * n_slots:]
